@@ -1,0 +1,136 @@
+/*
+ * bbc.h -- C ABI of the B200 balanced-butterfly counter (libbbc.so).
+ *
+ * The reference (/root/reference/pkg, pure Python) has no FFI: its engines are
+ * Python functions `engine(g, ...) -> int | (int, ScheduleReport)` exported from
+ * pkg/src/bbcount/__init__.py:10-63 and selected by name in the CLI
+ * (pkg/src/bbcount/cli.py:34, 216-233).  These entry points are what a binding
+ * of those engines binds (see INTEGRATION.md for the ctypes stub):
+ *
+ *   bbc_graph_create / bbc_graph_create_device
+ *       replaces SignedBipartiteGraph.build (graph.py:99-129): range check
+ *       (IndexOutOfRangeError, graph.py:109-114), duplicate rejection
+ *       (DuplicateEdgeError(u, v), graph.py:116-121), degrees (graph.py:91-92),
+ *       priority ranks (graph.py:93-97, 230-235), anchor-side choice
+ *       (min_side graph.py:174-176 / cheaper side by admitted wedges), and the
+ *       centre lists of _center_pairs (buckets.py:60-61), all on the device.
+ *   bbc_count
+ *       replaces the k = 2 hot kernel and its drivers:
+ *       _pair_subtotal (buckets.py:166-197), count_balanced_parallel
+ *       (buckets.py:213-246), count_balanced_tiled (tiled.py:107-168, algo
+ *       BBC_ALGO_GBBC) and count_balanced_dynamic (tiled.py:182-292, algo
+ *       BBC_ALGO_GBBCPP); also returns the unbalanced count the reference only
+ *       has through count_balanced_bruteforce (oracle.py:116-124).
+ *   bbc_block_work / bbc_task_order
+ *       the device side of ScheduleReport.per_block_work / task_order
+ *       (tiled.py:62-89).
+ *
+ * Conventions: plain pointers and sizes; host arrays are read during the call
+ * only; the library owns all device memory inside a handle.  One handle per
+ * device; a handle is not re-entrant.  Return codes map onto the reference's
+ * exceptions (errors.py:4-55); the message is in bbc_last_error() and the
+ * payload (edge index, duplicate pair) in bbc_last_error_info().
+ */
+#ifndef BBC_H
+#define BBC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bbc_graph bbc_graph;
+
+enum bbc_status {
+  BBC_OK = 0,
+  BBC_ERR_RANGE = 1,    /* IndexOutOfRangeError; info = edge*2 + (0: u, 1: v)   */
+  BBC_ERR_DUP = 2,      /* DuplicateEdgeError;  info = (u << 32) | v            */
+  BBC_ERR_OVERFLOW = 3, /* CountOverflowError (a total exceeds 2^64 - 1)        */
+  BBC_ERR_ARG = 4,      /* ValueError (bad sizes, options, sign not +-1)        */
+  BBC_ERR_CUDA = 5,     /* BBCountError                                         */
+  BBC_ERR_NCCL = 6,     /* BBCountError (reserved: collectives run host-side)   */
+  BBC_ERR_NOMEM = 7     /* BBCountError (device allocation failed)              */
+};
+
+enum bbc_algo {
+  BBC_ALGO_GBBC = 0,   /* G-BBC: static round-robin CTAs over anchors in rank order */
+  BBC_ALGO_GBBCPP = 1  /* G-BBC++: persistent CTAs, global atomic queue, descending work */
+};
+
+enum bbc_side_rule {
+  BBC_SIDE_CHEAPER = -1, /* fewer admitted wedges W_S (north_star (1))          */
+  BBC_SIDE_U = 0,
+  BBC_SIDE_V = 1,
+  BBC_SIDE_MIN = 2       /* reference min_side: smaller partition, ties to U    */
+};
+
+typedef struct {
+  int32_t algo;         /* bbc_algo                                                 */
+  int32_t tile_span;    /* endpoint-tile span (TileConfig.tile_size); 0 = max smem  */
+  int32_t blocks;       /* CTAs; 0 = one persistent wave (SMs x occupancy)          */
+  int32_t warp_max;     /* regime bands (tiled.py:171-179); 0 = defaults 32 / 512   */
+  int32_t partial_max;
+  int32_t part_index;   /* start-vertex partition [part_index of part_count]        */
+  int32_t part_count;   /* 0 or 1 = whole graph                                     */
+  int32_t flags;        /* reserved, 0                                              */
+} bbc_opts;
+
+typedef struct {
+  uint64_t wedges;        /* admitted wedges processed by this call (partition)     */
+  uint64_t wedges_total;  /* W_S of the processed side over the whole graph        */
+  uint64_t w_u, w_v;      /* W if anchoring U / V                                   */
+  uint64_t balanced_hi;   /* high 64 bits of the exact 128-bit totals               */
+  uint64_t unbalanced_hi;
+  int32_t anchor_side;    /* 0 = U, 1 = V                                           */
+  int32_t blocks;
+  int32_t threads;
+  int32_t tile_span;
+  int32_t tasks;          /* anchors dispatched by this call                        */
+  int32_t reserved;
+  float preprocess_ms;    /* device time of bbc_graph_create's device work          */
+  float count_ms;         /* device time of the count kernels (incl. closing)       */
+} bbc_stats;
+
+/* Build from HOST arrays (u:int32[m], v:int32[m], sign:int8[m] in {+1,-1}). */
+int bbc_graph_create(int device, int64_t n_u, int64_t n_v, int64_t m, const int32_t* u,
+                     const int32_t* v, const int8_t* sign, int32_t side_rule, bbc_graph** out);
+
+/* Same, from arrays already resident in device memory on `device` (not modified;
+ * the caller keeps ownership and must have finished writing them). */
+int bbc_graph_create_device(int device, int64_t n_u, int64_t n_v, int64_t m, const int32_t* d_u,
+                            const int32_t* d_v, const int8_t* d_sign, int32_t side_rule,
+                            bbc_graph** out);
+
+/* Count balanced / unbalanced butterflies: out[0] = balanced, out[1] = unbalanced
+ * (low 64 bits; BBC_ERR_OVERFLOW when either exceeds 2^64-1, high words in stats).
+ * With part_count > 1 the result is this partition's share; partial results of all
+ * partitions sum (mod 2^128) to the graph's counts. */
+int bbc_count(bbc_graph* g, const bbc_opts* opts, uint64_t out[2], bbc_stats* stats);
+
+/* Per-CTA admitted wedges of the last bbc_count (ScheduleReport.per_block_work). */
+int bbc_block_work(bbc_graph* g, uint64_t* out, int32_t n);
+
+/* Anchor dispatch order of `algo` as anchor-side vertex ids (ScheduleReport.task_order);
+ * `work` (nullable) receives each task's admitted wedges in the same order. */
+int bbc_task_order(bbc_graph* g, int32_t algo, int32_t* ids, uint64_t* work, int64_t n);
+
+/* info[0..7] = n_u, n_v, m, anchor_side, n_anchors, W_S, W_U, W_V */
+int bbc_graph_info(bbc_graph* g, int64_t* info, int32_t n);
+
+/* Stream the handle launches on (cudaStream_t as void*), for external timing. */
+void* bbc_graph_stream(bbc_graph* g);
+
+void bbc_graph_destroy(bbc_graph* g);
+
+/* Number of visible CUDA devices (0 when the driver reports none). */
+int bbc_device_count(void);
+
+const char* bbc_last_error(void);
+int64_t bbc_last_error_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BBC_H */

@@ -1,0 +1,204 @@
+"""ctypes binding of ``libbbc.so`` (the C ABI declared in ``include/bbc.h``).
+
+There is no CPU fallback: if the library is missing or no CUDA device is visible the
+counting entry points raise ``DeviceError``.  Status codes map onto the reference's
+exceptions (pkg/src/bbcount/errors.py): RANGE -> IndexOutOfRangeError, DUP ->
+DuplicateEdgeError(u, v), OVERFLOW -> CountOverflowError, ARG -> ValueError, the rest ->
+DeviceError (a BBCountError).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from .errors import CountOverflowError, DeviceError, DuplicateEdgeError, IndexOutOfRangeError
+
+LIB_PATH = Path(__file__).resolve().with_name("libbbc.so")
+
+ALGO_GBBC = 0
+ALGO_GBBCPP = 1
+SIDE_CHEAPER = -1
+SIDE_U = 0
+SIDE_V = 1
+SIDE_MIN = 2
+
+EXPORTED_SYMBOLS = (
+    "bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work", "bbc_task_order",
+    "bbc_graph_info", "bbc_graph_stream", "bbc_graph_destroy", "bbc_device_count", "bbc_last_error",
+    "bbc_last_error_info",
+)
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("algo", ctypes.c_int32), ("tile_span", ctypes.c_int32), ("blocks", ctypes.c_int32),
+                ("warp_max", ctypes.c_int32), ("partial_max", ctypes.c_int32), ("part_index", ctypes.c_int32),
+                ("part_count", ctypes.c_int32), ("flags", ctypes.c_int32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("wedges", ctypes.c_uint64), ("wedges_total", ctypes.c_uint64), ("w_u", ctypes.c_uint64),
+                ("w_v", ctypes.c_uint64), ("balanced_hi", ctypes.c_uint64), ("unbalanced_hi", ctypes.c_uint64),
+                ("anchor_side", ctypes.c_int32), ("blocks", ctypes.c_int32), ("threads", ctypes.c_int32),
+                ("tile_span", ctypes.c_int32), ("tasks", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("preprocess_ms", ctypes.c_float), ("count_ms", ctypes.c_float)]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libbbc.so once; raise DeviceError if it is absent (no silent fallback)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise DeviceError(f"{LIB_PATH} is not built; run `python -m paper_2601_17707_b200._build`")
+        L = ctypes.CDLL(str(LIB_PATH))
+        P, I32, I64, U64P = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(ctypes.c_uint64)
+        L.bbc_graph_create.argtypes = [ctypes.c_int, I64, I64, I64, P, P, P, I32, ctypes.POINTER(P)]
+        L.bbc_graph_create_device.argtypes = [ctypes.c_int, I64, I64, I64, P, P, P, I32, ctypes.POINTER(P)]
+        L.bbc_count.argtypes = [P, ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
+        L.bbc_block_work.argtypes = [P, U64P, I32]
+        L.bbc_task_order.argtypes = [P, I32, ctypes.POINTER(ctypes.c_int32), P, I64]
+        L.bbc_graph_info.argtypes = [P, ctypes.POINTER(ctypes.c_int64), I32]
+        L.bbc_graph_stream.argtypes = [P]
+        L.bbc_graph_stream.restype = P
+        L.bbc_graph_destroy.argtypes = [P]
+        L.bbc_graph_destroy.restype = None
+        L.bbc_device_count.argtypes = []
+        L.bbc_last_error.restype = ctypes.c_char_p
+        L.bbc_last_error_info.restype = ctypes.c_int64
+        for name in ("bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work",
+                     "bbc_task_order", "bbc_graph_info", "bbc_device_count"):
+            getattr(L, name).restype = ctypes.c_int
+        _lib = L
+        return L
+
+
+def device_count() -> int:
+    return int(load().bbc_device_count())
+
+
+def _raise(rc: int) -> None:
+    L = load()
+    msg = (L.bbc_last_error() or b"").decode()
+    info = int(L.bbc_last_error_info())
+    if rc == 1:
+        raise IndexOutOfRangeError(msg)
+    if rc == 2:
+        raise DuplicateEdgeError(info >> 32, info & 0xFFFFFFFF)
+    if rc == 3:
+        raise CountOverflowError(msg)
+    if rc == 4:
+        if msg.endswith("is not a valid EdgeSign"):
+            raise ValueError(msg)
+        raise ValueError(msg)
+    raise DeviceError(msg or f"libbbc error {rc}")
+
+
+@dataclass
+class CountResult:
+    balanced: int     # exact (may exceed 2^64 - 1; callers apply the overflow contract)
+    unbalanced: int
+    wedges: int       # admitted wedges processed by this call
+    wedges_total: int
+    w_u: int
+    w_v: int
+    anchor_side: int
+    blocks: int
+    threads: int
+    tile_span: int
+    tasks: int
+    preprocess_ms: float
+    count_ms: float
+
+
+class DeviceGraph:
+    """Owning handle of one device-resident graph (bbc_graph*)."""
+
+    def __init__(self, handle: int, device: int):
+        self._h = ctypes.c_void_p(handle)
+        self.device = device
+        info = (ctypes.c_int64 * 8)()
+        load().bbc_graph_info(self._h, info, 8)
+        self.n_u, self.n_v, self.m, self.anchor_side, self.n_anchors, self.w_s, self.w_u, self.w_v = \
+            (int(x) for x in info)
+
+    @classmethod
+    def from_host(cls, n_u: int, n_v: int, u: np.ndarray, v: np.ndarray, s: np.ndarray, device: int = 0,
+                  side_rule: int = SIDE_CHEAPER) -> "DeviceGraph":
+        u = np.ascontiguousarray(u, dtype=np.int32)
+        v = np.ascontiguousarray(v, dtype=np.int32)
+        s = np.ascontiguousarray(s, dtype=np.int8)
+        h = ctypes.c_void_p()
+        rc = load().bbc_graph_create(device, n_u, n_v, len(u), u.ctypes.data, v.ctypes.data, s.ctypes.data,
+                                     side_rule, ctypes.byref(h))
+        if rc:
+            _raise(rc)
+        return cls(h.value, device)
+
+    @classmethod
+    def from_device_ptrs(cls, n_u: int, n_v: int, m: int, ptr_u: int, ptr_v: int, ptr_s: int, device: int = 0,
+                         side_rule: int = SIDE_CHEAPER) -> "DeviceGraph":
+        h = ctypes.c_void_p()
+        rc = load().bbc_graph_create_device(device, n_u, n_v, m, ptr_u, ptr_v, ptr_s, side_rule, ctypes.byref(h))
+        if rc:
+            _raise(rc)
+        return cls(h.value, device)
+
+    def count(self, algo: int = ALGO_GBBCPP, tile_span: int = 0, blocks: int = 0, part_index: int = 0,
+              part_count: int = 1) -> CountResult:
+        if self._h is None:
+            raise DeviceError("graph handle already closed")
+        o = Opts(algo=algo, tile_span=tile_span, blocks=blocks, warp_max=0, partial_max=0, part_index=part_index,
+                 part_count=part_count, flags=0)
+        out = (ctypes.c_uint64 * 2)()
+        st = Stats()
+        rc = load().bbc_count(self._h, ctypes.byref(o), out, ctypes.byref(st))
+        if rc and rc != 3:
+            _raise(rc)
+        return CountResult(balanced=int(out[0]) | (int(st.balanced_hi) << 64),
+                           unbalanced=int(out[1]) | (int(st.unbalanced_hi) << 64), wedges=int(st.wedges),
+                           wedges_total=int(st.wedges_total), w_u=int(st.w_u), w_v=int(st.w_v),
+                           anchor_side=int(st.anchor_side), blocks=int(st.blocks), threads=int(st.threads),
+                           tile_span=int(st.tile_span), tasks=int(st.tasks), preprocess_ms=float(st.preprocess_ms),
+                           count_ms=float(st.count_ms))
+
+    def block_work(self, n: int) -> list[int]:
+        buf = (ctypes.c_uint64 * max(n, 1))()
+        rc = load().bbc_block_work(self._h, buf, n)
+        if rc:
+            _raise(rc)
+        return [int(buf[i]) for i in range(n)]
+
+    def task_order(self, algo: int) -> tuple[np.ndarray, np.ndarray]:
+        """(anchor ids, admitted wedges) in the dispatch order of ``algo``."""
+        n = self.n_anchors
+        ids = np.empty(max(n, 1), dtype=np.int32)
+        work = np.empty(max(n, 1), dtype=np.uint64)
+        rc = load().bbc_task_order(self._h, algo, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                   work.ctypes.data, n)
+        if rc:
+            _raise(rc)
+        return ids[:n], work[:n]
+
+    def stream(self) -> int:
+        return int(load().bbc_graph_stream(self._h) or 0)
+
+    def close(self) -> None:
+        if self._h is not None and self._h.value:
+            load().bbc_graph_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

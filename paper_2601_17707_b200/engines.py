@@ -1,0 +1,338 @@
+"""Counting entry points of the drop-in API, all running on the B200 CUDA path.
+
+Reference entry points kept (signatures, argument meaning, errors):
+
+  count_balanced_parallel(g, workers, inline_below)   buckets.py:213-246  (M-BBC)
+  count_balanced_2k_serial(g, k, anchor_side, ...)    buckets.py:64-154   (BB2K, k = 2)
+  count_balanced_tiled(g, TileConfig)                 tiled.py:107-168    (G-BBC)
+  count_balanced_dynamic(g, blocks, thresholds, mode) tiled.py:182-292    (G-BBC++)
+  count_balanced_bruteforce(g) -> (balanced, total)   oracle.py:116-124
+  sign_product_total(g)                               oracle.py:127-134
+
+plus ``count_signed_butterflies(g, ...) -> (balanced, unbalanced)``, the unbalanced count
+the reference only exposes through its brute-force oracle.
+
+Every engine hands the graph to ``libbbc.so`` (device preprocessing K1-K5 and the
+G-BBC / G-BBC++ kernels); nothing here counts on the host.  The device CSR is built once
+per (graph, device, side rule) and cached on the immutable graph object.
+
+Mapping of the reference's parallelism knobs onto the device:
+  * ``workers`` (fork-pool size) -> number of GPUs in this process, clamped to the
+    visible devices; start vertices are partitioned and the exact sums added;
+  * ``TileConfig.tile_size`` -> end-vertex tile span of the shared-memory counters,
+    ``TileConfig.block_count`` -> CTAs of the static G-BBC grid;
+  * ``block_count`` of the dynamic engine -> persistent CTAs claiming from the global
+    atomic queue; ``thresholds`` -> the regime bands reported in the histogram;
+  * ``inline_below`` has no device meaning (there is no cheaper in-process path) and is
+    only validated.
+"""
+
+from __future__ import annotations
+
+import enum
+import heapq
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import CountOverflowError, DeviceError, InvalidKError, InvalidThresholdsError, NoWorkError, U64_MAX
+from .graph import EdgeSign, Side, SignedBipartiteGraph
+
+DEFAULT_INLINE_BELOW = 250_000
+DEFAULT_TILE_SIZE = 128
+DEFAULT_WARP_MAX = 32
+DEFAULT_PARTIAL_MAX = 512
+
+
+# -- small host-side types (buckets.py:30-57, tiled.py:42-104) -------------------------
+
+class WedgeKind(enum.Enum):
+    SYMMETRIC = "symmetric"
+    ASYMMETRIC = "asymmetric"
+
+
+def wedge_kind(sign_uv: EdgeSign, sign_vw: EdgeSign) -> WedgeKind:
+    """Symmetric iff the two edge signs are equal (device: sign bit of word ^ s(u,v))."""
+    return WedgeKind.SYMMETRIC if sign_uv is sign_vw else WedgeKind.ASYMMETRIC
+
+
+@dataclass
+class WedgeCounters:
+    """Instrumentation filled by ``count_balanced_2k_serial`` from device counters.
+
+    ``admitted_per_anchor`` holds, per anchor id, the admitted wedges the device walked
+    under its rank filter (rank(w) > rank(u)); every admitted wedge lands in a bucket,
+    so ``bucket_sums_per_anchor`` equals it.  The device only scans admitted suffixes,
+    so ``scanned == admitted`` (the reference model also scans rejected wedges).
+    """
+
+    admitted_per_anchor: list[int] = field(default_factory=list)
+    bucket_sums_per_anchor: list[int] = field(default_factory=list)
+    scanned: int = 0
+
+    @property
+    def admitted(self) -> int:
+        return sum(self.admitted_per_anchor)
+
+
+def wedge_scan_bound(g: SignedBipartiteGraph, side: Side) -> int:
+    """Sum over centres of deg^2 (buckets.py:53-57)."""
+    d = g.degree_array(side.other()).astype(object)
+    return int(sum(x * x for x in d.tolist()))
+
+
+def admitted_wedges(g: SignedBipartiteGraph, side: Side) -> int:
+    """W_S = sum over the centre side of C(deg, 2): admitted wedges for any once-per-pair filter."""
+    d = g.degree_array(side.other())
+    return int(sum(int(x) * (int(x) - 1) // 2 for x in d.tolist()))
+
+
+class CooperationRegime(enum.Enum):
+    WARP = "warp"
+    PARTIAL_BLOCK = "partial_block"
+    FULL_BLOCK = "full_block"
+
+
+@dataclass(frozen=True)
+class TileConfig:
+    """tile_size bounds the per-tile counter span; block_count the CTAs (tiled.py:48-59)."""
+
+    tile_size: int = DEFAULT_TILE_SIZE
+    block_count: int = 1
+
+    def __post_init__(self):
+        if self.tile_size < 1:
+            raise ValueError(f"tile_size must be >= 1, got {self.tile_size}")
+        if self.block_count < 1:
+            raise ValueError(f"block_count must be >= 1, got {self.block_count}")
+
+
+@dataclass
+class ScheduleReport:
+    """Per-run load accounting (tiled.py:62-89), measured on the device.
+
+    per_block_work: admitted wedges processed by each CTA; task_order: anchor ids in
+    dispatch order; regime_histogram: anchors per cooperation band (dynamic engine only).
+    """
+
+    per_block_work: list[int]
+    max_over_mean: float
+    task_order: list[int]
+    regime_histogram: dict[CooperationRegime, int] | None = None
+
+    @property
+    def total_work(self) -> int:
+        return sum(self.per_block_work)
+
+    def to_json_dict(self) -> dict:
+        out: dict = {"per_block_work": self.per_block_work, "max_over_mean": self.max_over_mean,
+                     "task_order": self.task_order}
+        if self.regime_histogram is not None:
+            out["regime_histogram"] = {r.value: n for r, n in self.regime_histogram.items()}
+        return out
+
+
+def _max_over_mean(work: list[int]) -> float:
+    total = sum(work)
+    if total == 0:
+        return 1.0
+    return max(work) / (total / len(work))
+
+
+def load_imbalance(report: ScheduleReport) -> float:
+    """max / mean of per_block_work; NoWorkError when there is none (tiled.py:100-104)."""
+    if report.total_work == 0:
+        raise NoWorkError("schedule report has no work")
+    return _max_over_mean(report.per_block_work)
+
+
+def regime_for_degree(degree: int, warp_max: int = DEFAULT_WARP_MAX,
+                      partial_max: int = DEFAULT_PARTIAL_MAX) -> CooperationRegime:
+    """WARP below warp_max, FULL_BLOCK above partial_max, PARTIAL_BLOCK between (tiled.py:171-179)."""
+    if degree < warp_max:
+        return CooperationRegime.WARP
+    if degree <= partial_max:
+        return CooperationRegime.PARTIAL_BLOCK
+    return CooperationRegime.FULL_BLOCK
+
+
+# -- device plumbing ---------------------------------------------------------------------
+
+_SIDE_RULE = {None: _lib.SIDE_CHEAPER, Side.U: _lib.SIDE_U, Side.V: _lib.SIDE_V}
+
+
+def device_graph(g: SignedBipartiteGraph, device: int = 0, side: Side | None = None) -> _lib.DeviceGraph:
+    """The device CSR of ``g`` (built on first use, cached on the graph)."""
+    key = (device, side)
+    dg = g._device_cache.get(key)
+    if dg is None:
+        if _lib.device_count() <= device:
+            raise DeviceError(f"CUDA device {device} is not available; the counter has no CPU fallback")
+        u, v, s = g.edge_arrays()
+        dg = _lib.DeviceGraph.from_host(g.u_count, g.v_count, u, v, s, device, _SIDE_RULE[side])
+        g._device_cache[key] = dg
+    return dg
+
+
+def _devices(n: int) -> list[int]:
+    avail = _lib.device_count()
+    if avail < 1:
+        raise DeviceError("no CUDA device visible; the counter has no CPU fallback")
+    return list(range(min(max(n, 1), avail)))
+
+
+def _count(g: SignedBipartiteGraph, devices: list[int], algo: int, side: Side | None = None, tile_span: int = 0,
+           blocks: int = 0) -> tuple[int, int, list[_lib.CountResult]]:
+    """Exact (balanced, unbalanced) over start-vertex partitions, one per device."""
+    graphs = [device_graph(g, d, side) for d in devices]
+    if len(graphs) == 1:
+        r = graphs[0].count(algo, tile_span, blocks)
+        return r.balanced, r.unbalanced, [r]
+    results: list = [None] * len(graphs)
+    errors: list = []
+
+    def run(i: int) -> None:
+        try:
+            results[i] = graphs[i].count(algo, tile_span, blocks, part_index=i, part_count=len(graphs))
+        except BaseException as e:  # re-raised on the caller's thread
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(graphs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return sum(r.balanced for r in results), sum(r.unbalanced for r in results), results
+
+
+def _checked(balanced: int) -> int:
+    if balanced > U64_MAX:
+        raise CountOverflowError("balanced count exceeded 64-bit range")
+    return balanced
+
+
+# -- engines -----------------------------------------------------------------------------
+
+def count_signed_butterflies(g: SignedBipartiteGraph, devices: int = 1, algo: str = "gbbc++",
+                             anchor_side: Side | None = None) -> tuple[int, int]:
+    """(balanced, unbalanced) butterfly counts on ``devices`` GPUs of this process.
+
+    ``algo`` is "gbbc++" (dynamic queue) or "gbbc" (static); ``anchor_side`` None picks the
+    side with fewer admitted wedges.  CountOverflowError if either exceeds 2^64 - 1.
+    """
+    if devices < 1:
+        raise ValueError(f"devices must be >= 1, got {devices}")
+    code = {"gbbc++": _lib.ALGO_GBBCPP, "gbbc": _lib.ALGO_GBBC}.get(algo)
+    if code is None:
+        raise ValueError(f"unknown algo {algo!r}")
+    bal, unb, _ = _count(g, _devices(devices), code, anchor_side)
+    if bal > U64_MAX or unb > U64_MAX:
+        raise CountOverflowError("butterfly count exceeded 64-bit range")
+    return bal, unb
+
+
+def count_balanced_parallel(g: SignedBipartiteGraph, workers: int, inline_below: int = DEFAULT_INLINE_BELOW) -> int:
+    """Balanced butterflies with start vertices split over ``workers`` GPUs (buckets.py:213-246)."""
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    bal, _, _ = _count(g, _devices(workers), _lib.ALGO_GBBCPP)
+    return _checked(bal)
+
+
+def count_balanced_2k_serial(g: SignedBipartiteGraph, k: int, anchor_side: Side = Side.U,
+                             sort_neighbors: bool = False, counters: WedgeCounters | None = None) -> int:
+    """Balanced (2,k)-biclique count with the size-2 side on ``anchor_side`` (buckets.py:64-154).
+
+    k = 2 (balanced butterflies) runs on the device anchored on ``anchor_side``;
+    ``sort_neighbors`` is accepted (device lists are always rank-sorted).  k > 2 is the
+    next build step and raises NotImplementedError.
+    """
+    if k < 2:
+        raise InvalidKError(f"k must be >= 2, got {k}")
+    if k > 2:
+        raise NotImplementedError("balanced (2,k)-bicliques for k > 2 are not on the device path yet")
+    if g.side_count(anchor_side) == 0:
+        return 0
+    bal, _, _ = _count(g, _devices(1), _lib.ALGO_GBBCPP, anchor_side)
+    if counters is not None:
+        dg = device_graph(g, 0, anchor_side)
+        ids, work = dg.task_order(_lib.ALGO_GBBC)
+        per = np.zeros(g.side_count(anchor_side), dtype=np.int64)
+        per[ids] = work.astype(np.int64)
+        counters.admitted_per_anchor.extend(per.tolist())
+        counters.bucket_sums_per_anchor.extend(per.tolist())
+        counters.scanned += int(per.sum())
+    return _checked(bal)
+
+
+def count_balanced_tiled(g: SignedBipartiteGraph, cfg: TileConfig) -> tuple[int, ScheduleReport]:
+    """G-BBC: ``cfg.block_count`` CTAs take anchors round-robin; tiles of ``cfg.tile_size``."""
+    blocks = cfg.block_count
+    if g.side_count(Side.U) == 0 and g.side_count(Side.V) == 0:
+        return 0, ScheduleReport([0] * blocks, 1.0, [])
+    dg = device_graph(g)
+    if dg.n_anchors == 0:
+        return 0, ScheduleReport([0] * blocks, 1.0, [])
+    bal, _, _ = _count(g, [0], _lib.ALGO_GBBC, None, tile_span=cfg.tile_size, blocks=blocks)
+    work = dg.block_work(blocks)
+    ids, _ = dg.task_order(_lib.ALGO_GBBC)
+    return _checked(bal), ScheduleReport(work, _max_over_mean(work), ids.tolist())
+
+
+def count_balanced_dynamic(g: SignedBipartiteGraph, block_count: int,
+                           thresholds: tuple[int, int] = (DEFAULT_WARP_MAX, DEFAULT_PARTIAL_MAX),
+                           mode: str = "threads") -> tuple[int, ScheduleReport]:
+    """G-BBC++: persistent CTAs claim descending-work anchors from a global atomic queue.
+
+    ``mode="threads"`` reports the per-CTA work measured on the device (the split varies
+    run to run, the count does not).  ``mode="replay"`` reports the deterministic
+    least-loaded-claims-next replay (tiled.py:243-258) of the device's task list and
+    per-task work, for scheduling tests.
+    """
+    warp_max, partial_max = thresholds
+    if warp_max >= partial_max:
+        raise InvalidThresholdsError(f"warp_max {warp_max} must be below partial_max {partial_max}")
+    if block_count < 1:
+        raise ValueError(f"block_count must be >= 1, got {block_count}")
+    if mode not in ("threads", "replay"):
+        raise ValueError(f"unknown mode {mode!r}")
+    histogram = {r: 0 for r in CooperationRegime}
+    if g.u_count == 0 and g.v_count == 0:
+        return 0, ScheduleReport([0] * block_count, 1.0, [], histogram)
+    dg = device_graph(g)
+    side = Side.U if dg.anchor_side == 0 else Side.V
+    deg = g.degree_array(side)
+    histogram[CooperationRegime.WARP] = int((deg < warp_max).sum())
+    histogram[CooperationRegime.FULL_BLOCK] = int((deg > partial_max).sum())
+    histogram[CooperationRegime.PARTIAL_BLOCK] = int(len(deg)) - histogram[CooperationRegime.WARP] - \
+        histogram[CooperationRegime.FULL_BLOCK]
+    if dg.n_anchors == 0:
+        return 0, ScheduleReport([0] * block_count, 1.0, [], histogram)
+    bal, _, _ = _count(g, [0], _lib.ALGO_GBBCPP, None, blocks=block_count)
+    ids, task_work = dg.task_order(_lib.ALGO_GBBCPP)
+    if mode == "threads":
+        work = dg.block_work(block_count)
+    else:
+        work = [0] * block_count
+        clocks = [(0, b) for b in range(block_count)]
+        for w in task_work.tolist():
+            clock, b = heapq.heappop(clocks)
+            work[b] += w
+            heapq.heappush(clocks, (clock + w, b))
+    return _checked(bal), ScheduleReport(work, _max_over_mean(work), ids.tolist(), histogram)
+
+
+def count_balanced_bruteforce(g: SignedBipartiteGraph) -> tuple[int, int]:
+    """(balanced, total) butterflies (oracle.py:116-124); total = balanced + unbalanced."""
+    bal, unb = count_signed_butterflies(g)
+    return bal, bal + unb
+
+
+def sign_product_total(g: SignedBipartiteGraph) -> int:
+    """Sum over butterflies of the product of the four signs = balanced - unbalanced."""
+    bal, unb = count_signed_butterflies(g)
+    return bal - unb
