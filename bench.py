@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark: admitted wedges/sec of balanced/unbalanced butterfly counting on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): synthetic Chung-Lu signed bipartite graph, |U| = 1M,
+|V| = 500k, 20M distinct edges, 30 % negative (paper_2601_17707_b200/synth.py, seed 2).
+A "step" is one full count of the graph (G-BBC++ kernel incl. closing) with the CSR
+resident in HBM; under torchrun every rank holds the replicated CSR, counts its share of
+the start vertices and the counters are summed with one NCCL all-reduce.
+
+JSON line (rank 0): value = W_S / (max over ranks of the device-timed step), W_S the
+admitted wedges of the whole graph; `e2e` = the same metric through the public C ABI
+from pinned HOST edge arrays (upload + device preprocessing + count + result read-back
+per step); `roofline` for the count kernel; `cpu_baseline` = the CPU oracle port
+(oracle/bbc_oracle.c, restating the reference's bucket engine) on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "wedges/sec and end-to-end count time (device-timed) at 1/2/4/8 B200 vs CPU reference"
+UNIT = "wedges/s"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--algo", choices=("gbbc++", "gbbc"), default="gbbc++")
+    p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks() -> dict:
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = Path("/tmp") / f"bbc_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self) -> dict:
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = [r.split(", ") for r in self.path.read_text().strip().splitlines() if r.strip()]
+        rows = [r for r in rows if len(r) >= 9]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip().lower() == "active"})
+        loaded = [x for x in sm if x > 0.5 * max(mx or [1])] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_port_rate(n_u, n_v, u, v, s, budget_s: float, steps: int = 1, warmup: int = 0) -> dict:
+    """Time the oracle port (reference bucket engine restated in C) on a bounded anchor sample."""
+    from oracle.oracle import OracleGraph
+
+    threads = len(os.sched_getaffinity(0))
+    g = OracleGraph(n_u, n_v, u, v, s)
+    probe_stride = 997
+    t0 = time.perf_counter()
+    r = g.count(side=-1, threads=threads, stride=probe_stride)
+    t_probe = max(time.perf_counter() - t0, 1e-3)
+    est_full = t_probe * probe_stride
+    stride = max(1, int(est_full / max(budget_s, 1e-3)) + 1)
+    rates, adm = [], 0
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        r = g.count(side=-1, threads=threads, stride=stride)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            rates.append(r.admitted / dt)
+            adm = r.admitted
+    g.close()
+    cpu_model = ""
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                cpu_model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"value": statistics.median(rates), "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"anchors a with a % {stride} == 0 on the reference's min_side ({adm} admitted wedges, "
+                      f"reference filter prank[w] < prank[u]); graph build excluded as in cli.py:215",
+            "cpu": cpu_model, "stride": stride}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2601_17707_b200 import synth
+
+    cfg = synth.CONFIGS[args.config]
+    u, v, s = synth.generate(cfg)
+    budget = max(2.0, 150.0 / max(args.steps + args.warmup, 1))
+    cb = cpu_port_rate(cfg.n_u, cfg.n_v, u, v, s, budget, steps=args.steps, warmup=args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": cfg.name, "n_u": cfg.n_u, "n_v": cfg.n_v, "edges": cfg.m, "seed": cfg.seed},
+            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0},
+            "note": "reference = oracle/bbc_oracle.c, a C restatement of the reference's Python bucket engine "
+                    "(buckets.py:166-197) pinned to its golden vectors; the Python package is absent on this box"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_17707_b200 import _lib, synth
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = synth.CONFIGS[args.config]
+    u, v, s = synth.generate(cfg)
+    m = cfg.m
+
+    # ---- device-resident inputs: preprocessing once, then K timed count steps ----
+    du, dv, ds = (torch.from_numpy(x).cuda() for x in (u, v, s))
+    torch.cuda.synchronize()
+    g = _lib.DeviceGraph.from_device_ptrs(cfg.n_u, cfg.n_v, m, du.data_ptr(), dv.data_ptr(), ds.data_ptr(), local)
+    algo = _lib.ALGO_GBBCPP if args.algo == "gbbc++" else _lib.ALGO_GBBC
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    red = torch.zeros(6, dtype=torch.int64, device="cuda")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step():
+        flush.fill_(1)  # overwrite L2 between steps (outside the timed events)
+        torch.cuda.synchronize()
+        r = g.count(algo, part_index=rank, part_count=world)
+        ms = r.count_ms
+        if world > 1:
+            vals = [r.balanced & 0xFFFFFFFF, (r.balanced >> 32) & 0xFFFFFFFF, r.balanced >> 64,
+                    r.unbalanced & 0xFFFFFFFF, (r.unbalanced >> 32) & 0xFFFFFFFF, r.unbalanced >> 64]
+            red.copy_(torch.tensor(vals, dtype=torch.int64))
+            ev0.record()
+            dist.all_reduce(red)
+            ev1.record()
+            ev1.synchronize()
+            ms += ev0.elapsed_time(ev1)
+            t = red.tolist()
+            bal = t[0] + (t[1] << 32) + (t[2] << 64)
+            unb = t[3] + (t[4] << 32) + (t[5] << 64)
+        else:
+            bal, unb = r.balanced, r.unbalanced
+        return ms, bal, unb, r
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    times, results = [], None
+    with ClockSampler(local) as clocks:
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            ms, bal, unb, r = step()
+            times.append(ms)
+            results = (bal, unb, r)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        wall = time.perf_counter() - wall0
+    total_ms = sum(times)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    bal, unb, r = results
+    w_s = g.w_s
+    ms_per_step = total_ms / args.steps
+    value = w_s / (ms_per_step * 1e-3)
+    count_ms_local = sum(times) / args.steps
+
+    # ---- end-to-end through the public C ABI from pinned host buffers ----
+    pu = torch.from_numpy(u).pin_memory()
+    pv = torch.from_numpy(v).pin_memory()
+    ps = torch.from_numpy(s).pin_memory()
+    e2e_steps = args.e2e_steps or args.steps
+    e2e_times = []
+    e2e_launch = 0
+    for i in range(args.warmup + e2e_steps):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        h = ctypes_create(pu, pv, ps, cfg, local)
+        r2 = h.count(algo, part_index=rank, part_count=world)
+        if world > 1:
+            red.copy_(torch.tensor([r2.balanced & 0xFFFFFFFF, r2.balanced >> 32, 0, 0, 0, 0], dtype=torch.int64))
+            dist.all_reduce(red)
+            red.tolist()
+        dt = time.perf_counter() - t0
+        h.close()
+        if i >= args.warmup:
+            e2e_times.append(dt)
+    e2e_s = statistics.median(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_launch = 11  # own kernels per e2e step: 10 preprocessing + 1 count (CUB sort/scan kernels excluded)
+
+    # ---- roofline of the count kernel ----
+    peaks = measured_peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    n_s = g.n_anchors
+    alg_bytes = 4 * w_s + 12 * m + 8 * n_s
+    achieved = alg_bytes / (count_ms_local * 1e-3) / 1e9 / world if world > 1 else alg_bytes / (count_ms_local * 1e-3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "count_kernel_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(cfg.name)
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u32", "data": "synthetic",
+        "config": {"workload": cfg.name, "n_u": cfg.n_u, "n_v": cfg.n_v, "edges": m, "p_neg": cfg.p_neg,
+                   "gamma": cfg.gamma_u, "seed": cfg.seed, "anchor_side": "U" if g.anchor_side == 0 else "V",
+                   "W_S": w_s, "W_U": g.w_u, "W_V": g.w_v, "algo": args.algo,
+                   "parallelism": f"start-vertex partition x{world}, CSR replicated, NCCL all-reduce of counters",
+                   "l2": f"{L2_FLUSH_BYTES >> 20} MiB buffer overwritten between timed steps"},
+        "counts": {"balanced": bal, "unbalanced": unb, "total": bal + unb},
+        "count_ms": ms_per_step,
+        "preprocess_ms": r.preprocess_ms,
+        "wall_s_timed_region": wall,
+        "gpu_launches": args.steps,
+        "e2e": {"value": w_s / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 9 * m,
+                "d2h_bytes_per_step": 64 + 8 + 32 + 8 * r.blocks, "end_to_end_count_ms": e2e_s * 1e3,
+                "gpu_launches_per_step": e2e_launch, "path": "bbc_graph_create(host arrays) + bbc_count"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "algorithmic_bytes": alg_bytes,
+                     "bytes_model": "4*W_S + 12*|E| + 8*|S| (BASELINE.md 2)",
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650"},
+        "clocks": clocks.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_port_rate(cfg.n_u, cfg.n_v, u, v, s, args.cpu_seconds)
+    g.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def ctypes_create(pu, pv, ps, cfg, device):
+    from paper_2601_17707_b200 import _lib
+
+    import ctypes
+
+    h = ctypes.c_void_p()
+    rc = _lib.load().bbc_graph_create(device, cfg.n_u, cfg.n_v, cfg.m, pu.data_ptr(), pv.data_ptr(), ps.data_ptr(),
+                                      _lib.SIDE_CHEAPER, ctypes.byref(h))
+    if rc:
+        _lib._raise(rc)
+    return _lib.DeviceGraph(h.value, device)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

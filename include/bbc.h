@@ -73,7 +73,7 @@ typedef struct {
   int32_t partial_max;
   int32_t part_index;   /* start-vertex partition [part_index of part_count]        */
   int32_t part_count;   /* 0 or 1 = whole graph                                     */
-  int32_t flags;        /* reserved, 0                                              */
+  int32_t flags;        /* bit 0: general banded path only (testing)                */
 } bbc_opts;
 
 typedef struct {

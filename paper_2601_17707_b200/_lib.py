@@ -26,6 +26,7 @@ SIDE_CHEAPER = -1
 SIDE_U = 0
 SIDE_V = 1
 SIDE_MIN = 2
+FLAG_BANDED_ONLY = 1
 
 EXPORTED_SYMBOLS = (
     "bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work", "bbc_task_order",
@@ -154,11 +155,12 @@ class DeviceGraph:
         return cls(h.value, device)
 
     def count(self, algo: int = ALGO_GBBCPP, tile_span: int = 0, blocks: int = 0, part_index: int = 0,
-              part_count: int = 1) -> CountResult:
+              part_count: int = 1, flags: int = 0) -> CountResult:
+        """flags bit 0 (FLAG_BANDED_ONLY): always take the general banded path (testing)."""
         if self._h is None:
             raise DeviceError("graph handle already closed")
         o = Opts(algo=algo, tile_span=tile_span, blocks=blocks, warp_max=0, partial_max=0, part_index=part_index,
-                 part_count=part_count, flags=0)
+                 part_count=part_count, flags=flags)
         out = (ctypes.c_uint64 * 2)()
         st = Stats()
         rc = load().bbc_count(self._h, ctypes.byref(o), out, ctypes.byref(st))

@@ -4,20 +4,28 @@
 //   pkg/src/bbcount/buckets.py:166-197   per-anchor wedge buckets, filter, closing
 //   pkg/src/bbcount/tiled.py:107-168     G-BBC: static round-robin blocks, end-vertex
 //                                        tiles of bounded span (TileConfig.tile_size)
-//   pkg/src/bbcount/tiled.py:182-292     G-BBC++: fanout-sorted tasks claimed from a
+//   pkg/src/bbcount/tiled.py:182-292     G-BBC++: work-sorted tasks claimed from a
 //                                        shared counter by persistent workers
 //   PAPER.md:873-912 (Alg. 3), 1190-1253 (Alg. 4)
 //
-// One CTA processes one anchor (start vertex) u at a time.  For every record
-// (u, c) it walks the admitted suffix of centre c's rank-sorted list, i.e. the
-// wedges u -> c -> w with rank(w) > rank(u), and adds 1 to the positive or
-// negative half of w's packed u16x2 counter in a shared-memory tile over the
-// end-vertex rank range [lo, lo + span).  Parity = sign bit of (word ^ s(u,c)).
-// A tile is closed either by a sweep (balanced += C(p,2)+C(q,2), unbalanced +=
-// p*q, counter := 0) or, for sparse tiles, inline from the atomic's return value
-// (a + wedge adds the old positive count to balanced and the old negative count
-// to unbalanced, and vice versa; summed over all increments this equals the
-// sweep) followed by a re-walk that zeroes only the touched counters.
+// One CTA processes one anchor (start vertex) u at a time; several CTAs share an SM so
+// one anchor's barrier and load latency is covered by the others.  The wedges
+// u -> c -> w (rank(w) > rank(u)) are the admitted suffixes of the centres' rank-sorted
+// lists.  The end-vertex rank range is cut into bands of S ranks counted from the top
+// (band b = [n - (b+1) S, n - b S)), so the heavy high-degree end vertices share band 0.
+// Per band a shared-memory tile holds one packed counter per end vertex:
+//   W8  (deg u <= 255):   u8 positive | u8 negative, two end vertices per u32 word
+//   W16 (deg u <= 65535): u16 positive | u16 negative, one end vertex per word
+//   W32 (larger):         separate u32 positive / negative words
+// (a pair (u, w) has at most deg u common centres, so the halves never carry).  Each
+// wedge adds 1 to the positive or negative half, parity = sign bit of (word ^ s(u,c)).
+// A band is closed either by a sweep (balanced += C(p,2)+C(q,2), unbalanced += p*q,
+// counter := 0) when it holds at least as many wedges as counter words, or -- the usual
+// case -- inline from the atomic's return value (a + wedge adds the old positive count
+// to balanced and the old negative count to unbalanced, a - wedge the reverse; summed
+// over all increments this is exactly the sweep) followed by zeroing the touched words.
+// Sub-slices of each record within a band come from the band table (one load per edge
+// of the band) or, without a table, from a binary search.
 #include <algorithm>
 #include <string>
 
@@ -27,26 +35,28 @@ namespace bbc {
 
 namespace {
 
-constexpr int kCountThreads = 1024;
-constexpr int kWarps = kCountThreads / 32;
-constexpr int kRB = 2048;  // records per batch held in shared memory
 constexpr uint32_t kFull = 0xffffffffu;
 
-enum Mode { kDense = 0, kSparse = 1, kZero = 2, kWide = 3 };
+enum Mode { kDense = 0, kSparse = 1, kZero = 2 };
 
 struct Params {
   const uint32_t* __restrict__ adj;
   const uint2* __restrict__ rec;
+  const uint32_t* __restrict__ coff;
   const uint32_t* __restrict__ aoff;
   const unsigned long long* __restrict__ awork;
   const uint32_t* __restrict__ order;
+  const uint32_t* __restrict__ bnd;  // nullptr: binary search
+  uint32_t nbands;
   uint32_t n;
   uint32_t ntasks;
   uint32_t part_index;
   uint32_t part_count;
-  uint32_t span16;  // endpoint span of a packed tile
-  uint32_t span32;  // endpoint span of a wide (2 x u32) tile
+  uint32_t span8;   // band spans (end vertices per band) of the three layouts; with a
+  uint32_t span16;  // band table, span16 == table granularity and span8 == 2 * span16
+  uint32_t span32;
   uint32_t cap_words;
+  int fast;         // 0: always the general banded path (flags bit 0)
   int dynamic;
   unsigned long long* acc;
   unsigned int* queue;
@@ -63,10 +73,11 @@ __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
 
 // first position in [lo, hi) whose rank is >= x (lists are rank-sorted)
 __device__ __forceinline__ uint32_t lower_bound_rank(const uint32_t* __restrict__ adj, uint32_t lo, uint32_t hi,
-                                                     uint32_t x) {
+                                                     long long x) {
+  if (x <= 0) return lo;
   while (lo < hi) {
     uint32_t mid = (lo + hi) >> 1;
-    if ((__ldg(adj + mid) & 0x7fffffffu) < x)
+    if ((long long)(__ldg(adj + mid) & 0x7fffffffu) < x)
       lo = mid + 1;
     else
       hi = mid;
@@ -74,66 +85,48 @@ __device__ __forceinline__ uint32_t lower_bound_rank(const uint32_t* __restrict_
   return lo;
 }
 
-// exclusive scan of a[0..nb) in place; returns the total.  All threads call.
-__device__ uint32_t block_exclusive_scan(uint32_t* a, int nb, uint32_t* s_warp) {
-  constexpr int per = kRB / kCountThreads;
+// Block-wide exclusive scan of one u32 per thread fused with a u64 sum.
+template <int T>
+__device__ __forceinline__ uint32_t scan_sum(uint32_t v, unsigned long long w, uint32_t& total,
+                                             unsigned long long& wtotal, uint32_t* s_v, unsigned long long* s_w) {
+  constexpr int kWarps = T / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int base = threadIdx.x * per;
-  uint32_t v[per];
-  uint32_t sum = 0;
-#pragma unroll
-  for (int i = 0; i < per; ++i) {
-    v[i] = (base + i < nb) ? a[base + i] : 0u;
-    sum += v[i];
-  }
-  uint32_t x = sum;
+  uint32_t x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     uint32_t y = __shfl_up_sync(kFull, x, o);
     if (lane >= o) x += y;
   }
-  if (lane == 31) s_warp[warp] = x;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(kFull, w, o);
+  if (lane == 31) s_v[warp] = x;
+  if (lane == 0) s_w[warp] = w;
   __syncthreads();
   if (warp == 0) {
-    uint32_t w = s_warp[lane];
+    uint32_t a = lane < kWarps ? s_v[lane] : 0u;
+    unsigned long long b = lane < kWarps ? s_w[lane] : 0ull;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(kFull, w, o);
-      if (lane >= o) w += y;
+    for (int o = 1; o < kWarps; o <<= 1) {
+      uint32_t y = __shfl_up_sync(kFull, a, o);
+      if (lane >= o) a += y;
     }
-    s_warp[lane] = w;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(kFull, b, o);
+    if (lane < kWarps) s_v[lane] = a;
+    if (lane == 0) s_w[32] = b;
   }
   __syncthreads();
-  uint32_t excl = x - sum + (warp > 0 ? s_warp[warp - 1] : 0u);
-#pragma unroll
-  for (int i = 0; i < per; ++i) {
-    if (base + i < nb) a[base + i] = excl;
-    excl += v[i];
-  }
-  uint32_t total = s_warp[kWarps - 1];
-  __syncthreads();
-  return total;
+  total = s_v[kWarps - 1];
+  wtotal = s_w[32];
+  return x - v + (warp > 0 ? s_v[warp - 1] : 0u);
 }
 
-__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long x, unsigned long long* s_red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
-  if (lane == 0) s_red[warp] = x;
-  __syncthreads();
-  unsigned long long t = 0;
-#pragma unroll 4
-  for (int w = 0; w < kWarps; ++w) t += s_red[w];
-  __syncthreads();
-  return t;
-}
-
-// largest k in [0, nb) with pfx[k] <= ch
-__device__ __forceinline__ int find_record(const uint32_t* pfx, int nb, uint32_t ch) {
+// largest k in [0, nb) with pfx[k] <= g
+__device__ __forceinline__ int find_record(const uint32_t* pfx, int nb, uint32_t g) {
   int lo = 0, hi = nb;
   while (hi - lo > 1) {
     int mid = (lo + hi) >> 1;
-    if (pfx[mid] <= ch)
+    if (pfx[mid] <= g)
       lo = mid;
     else
       hi = mid;
@@ -141,78 +134,142 @@ __device__ __forceinline__ int find_record(const uint32_t* pfx, int nb, uint32_t
   return lo;
 }
 
-// Walk all chunks of the current record batch.  A chunk is 32 aligned int4
-// groups (128 adjacency words) of one record's sub-slice, one group per lane.
-template <int M>
-__device__ __forceinline__ void run_chunks(const Params& P, uint32_t* cnt, const uint32_t* s_sb,
-                                           const uint32_t* s_se, const uint32_t* s_pfx, int nb, uint32_t nchunks,
-                                           uint32_t lo, unsigned long long& tb, unsigned long long& tu) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+template <int W>
+__device__ __forceinline__ void bump(uint32_t* cnt, uint32_t rel, uint32_t par) {
+  if (W == 8) {
+    atomicAdd(&cnt[rel >> 1], 1u << (((rel & 1u) << 4) | (par << 3)));
+  } else if (W == 16) {
+    atomicAdd(&cnt[rel], 1u << (par << 4));
+  } else {
+    atomicAdd(&cnt[2u * rel + par], 1u);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void bump_close(uint32_t* cnt, uint32_t rel, uint32_t par, unsigned long long& tb,
+                                           unsigned long long& tu) {
+  if (W == 8) {
+    const uint32_t sh = ((rel & 1u) << 4) | (par << 3);
+    const uint32_t old = atomicAdd(&cnt[rel >> 1], 1u << sh);
+    tb += (old >> sh) & 0xffu;
+    tu += (old >> (sh ^ 8u)) & 0xffu;
+  } else {
+    const uint32_t sh = par << 4;
+    const uint32_t old = atomicAdd(&cnt[rel], 1u << sh);
+    tb += (old >> sh) & 0xffffu;
+    tu += (old >> (sh ^ 16u)) & 0xffffu;
+  }
+}
+
+// Walk the int4 groups of the batch's sub-slices, one group per thread.  Consecutive
+// threads take consecutive groups of the same record (coalesced 512 B per warp).
+template <int T, int W, int M>
+__device__ __forceinline__ void walk(const Params& P, uint32_t* cnt, const uint32_t* s_lo, const uint32_t* s_hi,
+                                     const uint32_t* s_pfx, int nb, uint32_t ngroups, uint32_t lo_rank,
+                                     unsigned long long& tb, unsigned long long& tu) {
   const uint4* adj4 = reinterpret_cast<const uint4*>(P.adj);
-  for (uint32_t ch = warp; ch < nchunks; ch += kWarps) {
-    const int k = find_record(s_pfx, nb, ch);
-    const uint32_t sbx = s_sb[k];
-    const uint32_t sb = sbx & 0x7fffffffu, sgn = sbx & 0x80000000u, se = s_se[k];
-    const uint32_t grp = (sb >> 2) + (ch - s_pfx[k]) * 32u + (uint32_t)lane;
-    const uint32_t p0 = grp * 4u;
-    if (p0 < se) {
-      const uint4 q = ld_stream(adj4 + grp);
-      const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+  for (uint32_t g = threadIdx.x; g < ngroups; g += T) {
+    const int k = find_record(s_pfx, nb, g);
+    const uint32_t lox = s_lo[k];
+    const uint32_t lo = lox & 0x7fffffffu, sgn = lox & 0x80000000u, hi = s_hi[k];
+    const uint32_t grp = (lo >> 2) + (g - s_pfx[k]);
+    const uint4 q = ld_stream(adj4 + grp);
+    const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+    const uint32_t p0 = grp << 2;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t p = p0 + (uint32_t)j;
-        if (p >= sb && p < se) {
-          const uint32_t word = wv[j];
-          const uint32_t idx = (word & 0x7fffffffu) - lo;
-          const uint32_t par = (word ^ sgn) >> 31;  // 1: asymmetric (negative) wedge
-          if (M == kDense) {
-            atomicAdd(&cnt[idx], par ? 0x10000u : 1u);
-          } else if (M == kWide) {
-            atomicAdd(&cnt[2u * idx + par], 1u);
-          } else if (M == kSparse) {
-            const uint32_t old = atomicAdd(&cnt[idx], par ? 0x10000u : 1u);
-            const uint32_t lo16 = old & 0xffffu, hi16 = old >> 16;
-            tb += par ? hi16 : lo16;
-            tu += par ? lo16 : hi16;
-          } else {  // kZero
-            cnt[idx] = 0u;
-          }
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t p = p0 + (uint32_t)j;
+      if (p >= lo && p < hi) {
+        const uint32_t word = wv[j];
+        const uint32_t rel = (word & 0x7fffffffu) - lo_rank;
+        const uint32_t par = (word ^ sgn) >> 31;  // 1: asymmetric (negative) wedge
+        if (M == kDense) {
+          bump<W>(cnt, rel, par);
+        } else if (M == kSparse) {
+          bump_close<W>(cnt, rel, par, tb, tu);
+        } else {
+          cnt[W == 8 ? (rel >> 1) : rel] = 0u;
         }
       }
     }
   }
 }
 
-// closing sweep of a packed tile: balanced += C(p,2)+C(q,2), unbalanced += p*q
-__device__ __forceinline__ void sweep16(uint32_t* cnt, uint32_t span, unsigned long long& tb,
-                                        unsigned long long& tu) {
-  uint4* c4 = reinterpret_cast<uint4*>(cnt);
-  const uint32_t nq = (span + 3) >> 2;
-  for (uint32_t i = threadIdx.x; i < nq; i += kCountThreads) {
-    uint4 x = c4[i];
-    if ((x.x | x.y | x.z | x.w) == 0u) continue;
-    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+// Sparse band walk with at most two int4 groups per thread: both loads are issued before
+// either group is processed, and the touched counter words are kept in registers so the
+// zeroing pass needs neither the adjacency nor the record search again.
+template <int T, int W>
+__device__ __forceinline__ void walk2_sparse(const Params& P, uint32_t* cnt, const uint32_t* s_lo,
+                                             const uint32_t* s_hi, const uint32_t* s_pfx, int nb, uint32_t ngroups,
+                                             uint32_t lo_rank, unsigned long long& tb, unsigned long long& tu,
+                                             uint32_t (&touched)[8]) {
+  const uint4* adj4 = reinterpret_cast<const uint4*>(P.adj);
+  uint4 q[2];
+  uint32_t lo[2], hi[2], sg[2], p0[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const uint32_t g = threadIdx.x + (uint32_t)i * T;
+    lo[i] = 1u;
+    hi[i] = 0u;
+    sg[i] = 0u;
+    p0[i] = 0u;
+    q[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (g < ngroups) {
+      const int k = find_record(s_pfx, nb, g);
+      const uint32_t lox = s_lo[k];
+      lo[i] = lox & 0x7fffffffu;
+      sg[i] = lox & 0x80000000u;
+      hi[i] = s_hi[k];
+      const uint32_t grp = (lo[i] >> 2) + (g - s_pfx[k]);
+      p0[i] = grp << 2;
+      q[i] = ld_stream(adj4 + grp);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const uint32_t wv[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const uint32_t p = xs[j] & 0xffffu, q = xs[j] >> 16;
-      tb += (unsigned long long)((p * (p - (p > 0))) >> 1) + (unsigned long long)((q * (q - (q > 0))) >> 1);
-      tu += (unsigned long long)(p * q);
+      const uint32_t p = p0[i] + (uint32_t)j;
+      touched[4 * i + j] = 0xffffffffu;
+      if (p >= lo[i] && p < hi[i]) {
+        const uint32_t rel = (wv[j] & 0x7fffffffu) - lo_rank;
+        bump_close<W>(cnt, rel, (wv[j] ^ sg[i]) >> 31, tb, tu);
+        touched[4 * i + j] = W == 8 ? (rel >> 1) : rel;
+      }
     }
-    c4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
-// closing sweep of a wide tile (interleaved u32 positive / negative counts)
-__device__ __forceinline__ void sweep32(uint32_t* cnt, uint32_t span, unsigned long long& tb,
-                                        unsigned long long& tu) {
+__device__ __forceinline__ unsigned long long c2(unsigned long long x) { return x * (x - (x > 0)) >> 1; }
+
+// closing sweep over `words` counter words of layout W
+template <int T, int W>
+__device__ __forceinline__ void sweep(uint32_t* cnt, uint32_t words, unsigned long long& tb, unsigned long long& tu) {
   uint4* c4 = reinterpret_cast<uint4*>(cnt);
-  const uint32_t nq = (2u * span + 3) >> 2;
-  for (uint32_t i = threadIdx.x; i < nq; i += kCountThreads) {
-    uint4 x = c4[i];
+  const uint32_t nq = (words + 3) >> 2;
+  for (uint32_t i = threadIdx.x; i < nq; i += T) {
+    const uint4 x = c4[i];
     if ((x.x | x.y | x.z | x.w) == 0u) continue;
-    const unsigned long long p0 = x.x, q0 = x.y, p1 = x.z, q1 = x.w;
-    tb += p0 * (p0 - (p0 > 0)) / 2 + q0 * (q0 - (q0 > 0)) / 2 + p1 * (p1 - (p1 > 0)) / 2 + q1 * (q1 - (q1 > 0)) / 2;
-    tu += p0 * q0 + p1 * q1;
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+    if (W == 8) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t p0 = xs[j] & 0xffu, q0 = (xs[j] >> 8) & 0xffu, p1 = (xs[j] >> 16) & 0xffu, q1 = xs[j] >> 24;
+        tb += (p0 * (p0 - (p0 > 0)) + q0 * (q0 - (q0 > 0)) + p1 * (p1 - (p1 > 0)) + q1 * (q1 - (q1 > 0))) >> 1;
+        tu += p0 * q0 + p1 * q1;
+      }
+    } else if (W == 16) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t p = xs[j] & 0xffffu, q = xs[j] >> 16;
+        tb += (unsigned long long)((p * (p - (p > 0))) >> 1) + (unsigned long long)((q * (q - (q > 0))) >> 1);
+        tu += (unsigned long long)(p * q);
+      }
+    } else {
+      tb += c2(xs[0]) + c2(xs[1]) + c2(xs[2]) + c2(xs[3]);
+      tu += (unsigned long long)xs[0] * xs[1] + (unsigned long long)xs[2] * xs[3];
+    }
     c4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
 }
@@ -222,93 +279,209 @@ __device__ __forceinline__ void add128(unsigned long long& lo, unsigned long lon
   hi += (lo < x) ? 1ull : 0ull;
 }
 
-__global__ void __launch_bounds__(kCountThreads, 1) k_count(Params P) {
-  extern __shared__ uint4 smem4[];
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem4);
-  uint32_t* s_sb = cnt + P.cap_words;
-  uint32_t* s_se = s_sb + kRB;
-  uint32_t* s_pfx = s_se + kRB;
-  __shared__ uint32_t s_warp[32];
-  __shared__ unsigned long long s_red[kWarps];
-  __shared__ uint32_t s_task;
+struct Smem {
+  uint32_t* cnt;
+  uint32_t* lo;
+  uint32_t* hi;
+  uint32_t* pfx;
+  uint32_t* v;
+  unsigned long long* w;
+};
 
-  for (uint32_t i = threadIdx.x; i < P.cap_words / 4; i += kCountThreads) smem4[i] = make_uint4(0u, 0u, 0u, 0u);
+// General path: any degree (records in batches of T), table or binary search, layout W.
+template <int T, int W>
+__device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint32_t rb, uint32_t re,
+                               unsigned long long& tb, unsigned long long& tu, unsigned long long& work) {
+  const uint32_t span = W == 8 ? P.span8 : (W == 16 ? P.span16 : P.span32);
+  const uint32_t step = W == 8 ? 2u : 1u;  // table columns per band
+  const bool table = P.bnd != nullptr && W != 32;
+  const uint32_t nbands_u = (P.n - 1u - r) / span + 1u;  // bands 0..nbands_u-1 hold ranks > r
+  const bool multi = (re - rb) > (uint32_t)T;
+  for (uint32_t b = 0; b < nbands_u; ++b) {
+    const long long top = (long long)P.n - (long long)b * span;
+    const long long bot = top - (long long)span;
+    const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
+    const uint32_t band_span = (uint32_t)(top - (long long)lo_rank);
+    const uint32_t band_words = W == 8 ? (band_span + 1u) / 2u : (W == 16 ? band_span : 2u * band_span);
+    int mode = -1;
+    unsigned long long band_w = 0;
+    for (uint32_t b0 = rb; b0 < re; b0 += T) {
+      const int nb = (int)min((uint32_t)T, re - b0);
+      uint32_t ng = 0;
+      unsigned long long myw = 0;
+      if ((int)threadIdx.x < nb) {
+        const uint2 rr = P.rec[b0 + threadIdx.x];
+        const uint32_t begin = rr.x & 0x7fffffffu, c = rr.y;
+        uint32_t lo, hi;
+        if (table) {
+          const uint32_t* row = P.bnd + (size_t)c * P.nbands;
+          const uint32_t j0 = b * step, j1 = (b + 1u) * step;
+          hi = __ldg(row + j0);
+          lo = j1 < P.nbands ? __ldg(row + j1) : 0u;
+        } else {
+          const uint32_t end = __ldg(P.coff + c + 1);
+          hi = b == 0 ? end : lower_bound_rank(P.adj, begin, end, top);
+          lo = lower_bound_rank(P.adj, begin, hi, bot);
+        }
+        lo = max(lo, begin);
+        hi = max(hi, lo);
+        if (hi > lo) {
+          ng = ((hi + 3u) >> 2) - (lo >> 2);
+          myw = hi - lo;
+        }
+        S.lo[threadIdx.x] = lo | (rr.x & 0x80000000u);
+        S.hi[threadIdx.x] = hi;
+      }
+      uint32_t ngroups;
+      unsigned long long bw;
+      const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w);
+      if ((int)threadIdx.x < nb) S.pfx[threadIdx.x] = ex;
+      __syncthreads();
+      work += myw;
+      band_w += bw;
+      // several record batches, or a W32 tile, are always closed by the sweep
+      if (mode < 0) mode = (W == 32 || multi || bw >= band_words) ? kDense : kSparse;
+      if (ngroups == 0) continue;
+      if (mode == kDense) {
+        walk<T, W, kDense>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
+      } else {
+        walk<T, W, kSparse>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
+        __syncthreads();
+        walk<T, W, kZero>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
+      }
+      __syncthreads();
+    }
+    if (mode == kDense && band_w > 0) {
+      sweep<T, W>(S.cnt, band_words, tb, tu);
+      __syncthreads();
+    }
+  }
+}
+
+// Anchors with deg <= T and a band table (layouts W8 / W16): the records stay in
+// registers for all bands, each band's lower table column is prefetched one band ahead,
+// sparse bands close inline (zeroing from registers when <= 2 groups per thread, else
+// by a re-walk), dense bands use a no-return increment and a closing sweep.
+template <int T, int W>
+__device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, uint32_t rb, uint32_t re,
+                                    unsigned long long& tb, unsigned long long& tu, unsigned long long& work) {
+  const uint32_t span = W == 8 ? P.span8 : P.span16;
+  const uint32_t step = W == 8 ? 2u : 1u;
+  const uint32_t nbu = (P.n - 1u - r) / span + 1u;
+  const int nb = (int)(re - rb);
+  const bool mine = (int)threadIdx.x < nb;
+  uint32_t recx = 0u, hi_next = 0u, lo_next = 0u;
+  const uint32_t* row = P.bnd;
+  if (mine) {
+    const uint2 rr = P.rec[rb + threadIdx.x];
+    recx = rr.x;
+    row = P.bnd + (size_t)rr.y * P.nbands;
+    hi_next = __ldg(row);
+    lo_next = step < P.nbands ? __ldg(row + step) : 0u;
+  }
+  for (uint32_t b = 0; b < nbu; ++b) {
+    const long long top = (long long)P.n - (long long)b * span;
+    const long long bot = top - (long long)span;
+    const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
+    const uint32_t band_span = (uint32_t)(top - (long long)lo_rank);
+    uint32_t ng = 0;
+    unsigned long long myw = 0;
+    if (mine) {
+      uint32_t hi = hi_next, lo = lo_next;
+      const uint32_t j2 = (b + 2u) * step;
+      hi_next = lo;
+      lo_next = (b + 1u < nbu && j2 < P.nbands) ? __ldg(row + j2) : 0u;  // prefetch for band b + 1
+      lo = max(lo, recx & 0x7fffffffu);
+      hi = max(hi, lo);
+      if (hi > lo) {
+        ng = ((hi + 3u) >> 2) - (lo >> 2);
+        myw = hi - lo;
+      }
+      S.lo[threadIdx.x] = lo | (recx & 0x80000000u);
+      S.hi[threadIdx.x] = hi;
+    }
+    uint32_t ngroups;
+    unsigned long long bw;
+    const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w);
+    if (mine) S.pfx[threadIdx.x] = ex;
+    __syncthreads();
+    work += myw;
+    if (ngroups == 0) continue;
+    const uint32_t band_words = W == 8 ? (band_span + 1u) / 2u : band_span;
+    if (ngroups <= 2u * T) {
+      uint32_t touched[8];
+      walk2_sparse<T, W>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu, touched);
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (touched[j] != 0xffffffffu) S.cnt[touched[j]] = 0u;
+      __syncthreads();
+    } else if (bw < band_words) {
+      walk<T, W, kSparse>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
+      __syncthreads();
+      walk<T, W, kZero>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
+      __syncthreads();
+    } else {
+      walk<T, W, kDense>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
+      __syncthreads();
+      sweep<T, W>(S.cnt, band_words, tb, tu);
+      __syncthreads();
+    }
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(T, 1024 / T) k_count(Params P) {
+  constexpr int kWarps = T / 32;
+  extern __shared__ uint4 smem4[];
+  __shared__ uint32_t s_v[32];
+  __shared__ unsigned long long s_w[33];
+  __shared__ uint32_t s_task;
+  Smem S;
+  S.cnt = reinterpret_cast<uint32_t*>(smem4);
+  S.lo = S.cnt + P.cap_words;
+  S.hi = S.lo + T;
+  S.pfx = S.hi + T;
+  S.v = s_v;
+  S.w = s_w;
+
+  for (uint32_t i = threadIdx.x; i < P.cap_words / 4; i += T) smem4[i] = make_uint4(0u, 0u, 0u, 0u);
 
   unsigned long long bal_lo = 0, bal_hi = 0, unb_lo = 0, unb_hi = 0, work = 0;
   uint32_t next = blockIdx.x;
+  if (threadIdx.x == 0) s_task = P.dynamic ? atomicAdd(P.queue, 1u) : next;
+  __syncthreads();
   for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_task = P.dynamic ? atomicAdd(P.queue, 1u) : next;
-    __syncthreads();
     const uint32_t t = s_task;
     next += gridDim.x;
+    __syncthreads();  // every thread holds t before s_task is overwritten
     if (t >= P.ntasks) break;
+    // claim the following task now so the queue round trip overlaps this anchor
+    if (threadIdx.x == 0) s_task = P.dynamic ? atomicAdd(P.queue, 1u) : next;
     const uint32_t gidx = P.part_index + t * P.part_count;
     const uint32_t r = P.dynamic ? P.order[gidx] : gidx;
-    if (P.awork[r] == 0ull) continue;
-    const uint32_t rb = P.aoff[r], re = P.aoff[r + 1];
-    const bool wide = (re - rb) > 65535u;  // counts are bounded by deg(u); u16 halves suffice below
-    const uint32_t span_cap = wide ? P.span32 : P.span16;
-    unsigned long long tb = 0, tu = 0;
-    for (uint32_t lo = r + 1; lo < P.n; lo += span_cap) {
-      const uint32_t hi = min(P.n, lo + span_cap);
-      const uint32_t span = hi - lo;
-      const bool first = lo == r + 1, last = hi == P.n;
-      int mode = -1;
-      unsigned long long tile_w = 0;
-      for (uint32_t b0 = rb; b0 < re; b0 += kRB) {
-        const int nb = (int)min((uint32_t)kRB, re - b0);
-        unsigned long long myw = 0;
-        for (int k = threadIdx.x; k < nb; k += kCountThreads) {
-          const uint2 rr = P.rec[b0 + k];
-          uint32_t sb = rr.x & 0x7fffffffu, se = rr.y;
-          if (!first) sb = lower_bound_rank(P.adj, sb, se, lo);
-          if (!last) se = lower_bound_rank(P.adj, sb, se, hi);
-          uint32_t nq = 0;
-          if (se > sb) {
-            nq = ((se + 3u) >> 2) - (sb >> 2);
-            myw += se - sb;
-          }
-          s_sb[k] = sb | (rr.x & 0x80000000u);
-          s_se[k] = se;
-          s_pfx[k] = (nq + 31u) >> 5;
-        }
-        __syncthreads();
-        const uint32_t nchunks = block_exclusive_scan(s_pfx, nb, s_warp);
-        const unsigned long long bw = block_sum_u64(myw, s_red);
-        work += myw;
-        tile_w += bw;
-        if (mode < 0) {
-          if (wide)
-            mode = kWide;
-          else if (re - rb > (uint32_t)kRB || 2ull * bw >= span)
-            mode = kDense;
-          else
-            mode = kSparse;
-        }
-        if (nchunks == 0) continue;
-        if (mode == kDense) {
-          run_chunks<kDense>(P, cnt, s_sb, s_se, s_pfx, nb, nchunks, lo, tb, tu);
-        } else if (mode == kWide) {
-          run_chunks<kWide>(P, cnt, s_sb, s_se, s_pfx, nb, nchunks, lo, tb, tu);
-        } else {
-          run_chunks<kSparse>(P, cnt, s_sb, s_se, s_pfx, nb, nchunks, lo, tb, tu);
-          __syncthreads();
-          run_chunks<kZero>(P, cnt, s_sb, s_se, s_pfx, nb, nchunks, lo, tb, tu);
-        }
-        __syncthreads();
-      }
-      if (tile_w == 0) continue;
-      if (mode == kDense) {
-        sweep16(cnt, span, tb, tu);
-        __syncthreads();
-      } else if (mode == kWide) {
-        sweep32(cnt, span, tb, tu);
-        __syncthreads();
-      }
+    const unsigned long long w_a = P.awork[r];
+    if (w_a == 0ull) {
+      __syncthreads();  // publish the claimed task
+      continue;
     }
+    const uint32_t rb = P.aoff[r], re = P.aoff[r + 1];
+    const uint32_t deg = re - rb;
+    unsigned long long tb = 0, tu = 0;
+    const bool fast = P.fast && P.bnd != nullptr && deg <= (uint32_t)T;
+    if (fast && deg <= 255u)
+      process_anchor_fast<T, 8>(P, S, r, rb, re, tb, tu, work);
+    else if (fast)
+      process_anchor_fast<T, 16>(P, S, r, rb, re, tb, tu, work);
+    else if (deg <= 255u)
+      process_anchor<T, 8>(P, S, r, rb, re, tb, tu, work);
+    else if (deg <= 65535u)
+      process_anchor<T, 16>(P, S, r, rb, re, tb, tu, work);
+    else
+      process_anchor<T, 32>(P, S, r, rb, re, tb, tu, work);
     add128(bal_lo, bal_hi, tb);
     add128(unb_lo, unb_hi, tu);
+    __syncthreads();  // publish the claimed task
   }
 
   // exact 128-bit reduction: warp shuffle, then one pair of global atomics per warp
@@ -317,32 +490,76 @@ __global__ void __launch_bounds__(kCountThreads, 1) k_count(Params P) {
   for (int o = 16; o; o >>= 1) {
     unsigned long long l2 = __shfl_xor_sync(kFull, bal_lo, o), h2 = __shfl_xor_sync(kFull, bal_hi, o);
     unsigned long long l3 = __shfl_xor_sync(kFull, unb_lo, o), h3 = __shfl_xor_sync(kFull, unb_hi, o);
+    unsigned long long w2 = __shfl_xor_sync(kFull, work, o);
     bal_lo += l2;
     bal_hi += h2 + (bal_lo < l2 ? 1ull : 0ull);
     unb_lo += l3;
     unb_hi += h3 + (unb_lo < l3 ? 1ull : 0ull);
+    work += w2;
   }
   if (lane == 0) {
     unsigned long long old = atomicAdd(&P.acc[0], bal_lo);
     atomicAdd(&P.acc[1], bal_hi + (old + bal_lo < old ? 1ull : 0ull));
     old = atomicAdd(&P.acc[2], unb_lo);
     atomicAdd(&P.acc[3], unb_hi + (old + unb_lo < old ? 1ull : 0ull));
+    s_w[threadIdx.x >> 5] = work;
   }
-  const unsigned long long bw = block_sum_u64(work, s_red);
-  if (threadIdx.x == 0) P.block_work[blockIdx.x] = bw;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kWarps; ++w) t += s_w[w];
+    P.block_work[blockIdx.x] = t;
+  }
 }
 
-int configure(Graph& g, int& cap_words, int& smem_bytes) {
+struct Launch {
+  int threads = 0;
+  int blocks_per_sm = 0;
+  int cap_words = 0;
+  int smem_bytes = 0;
+  void (*kernel)(Params) = nullptr;
+};
+
+template <int T>
+int configure_t(Graph& g, Launch& L) {
   cudaFuncAttributes fa;
-  BBC_CK(cudaFuncGetAttributes(&fa, k_count));
-  int avail = g.max_smem - (int)fa.sharedSizeBytes - 3 * kRB * 4 - 64;
-  cap_words = (avail / 16) * 4;
-  smem_bytes = cap_words * 4 + 3 * kRB * 4 + 16;
-  BBC_CK(cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  BBC_CK(cudaFuncGetAttributes(&fa, k_count<T>));
+  int per_sm = 0;
+  BBC_CK(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, g.device));
+  const int bps = 1024 / T;
+  // per-CTA budget: an equal share of the SM (1 KB per CTA is reserved by the driver)
+  int budget = std::min(g.max_smem, per_sm / bps - 1024);
+  int avail = budget - (int)fa.sharedSizeBytes - (3 * T * 4 + 64);
+  L.threads = T;
+  L.blocks_per_sm = bps;
+  L.cap_words = (avail / 16) * 4;
+  L.smem_bytes = L.cap_words * 4 + 3 * T * 4 + 16;
+  L.kernel = k_count<T>;
+  BBC_CK(cudaFuncSetAttribute(k_count<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes));
   return BBC_OK;
 }
 
+int configure(Graph& g, Launch& L) {
+  switch (g.threads) {
+    case 128:
+      return configure_t<128>(g, L);
+    case 256:
+      return configure_t<256>(g, L);
+    case 512:
+      return configure_t<512>(g, L);
+    default:
+      return configure_t<1024>(g, L);
+  }
+}
+
 }  // namespace
+
+int count_span16(Graph& g) {
+  Launch L;
+  BBC_CK(cudaSetDevice(g.device));
+  if (configure(g, L)) return -1;
+  return L.cap_words - 8;
+}
 
 int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
   bbc_opts opts{};
@@ -361,16 +578,21 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     return BBC_ERR_ARG;
   }
   BBC_CK(cudaSetDevice(g.device));
-  int cap_words = 0, smem_bytes = 0;
-  int rc = configure(g, cap_words, smem_bytes);
+  Launch L;
+  int rc = configure(g, L);
   if (rc) return rc;
-  uint32_t span16 = (uint32_t)cap_words - 4u;
-  uint32_t span32 = (uint32_t)cap_words / 2u - 4u;
-  if (opts.tile_span > 0) {
-    span16 = std::min<uint32_t>(span16, (uint32_t)opts.tile_span);
-    span32 = std::min<uint32_t>(span32, (uint32_t)opts.tile_span);
+  uint32_t span16 = (uint32_t)L.cap_words - 8u;
+  uint32_t span8 = 2u * span16, span32 = span16 / 2u;
+  bool use_table = g.bnd != nullptr && span16 == g.t16;
+  if (opts.tile_span > 0 && (uint32_t)opts.tile_span < span8) {
+    // TileConfig.tile_size: bands of at most tile_span end vertices in every layout
+    const uint32_t t = (uint32_t)opts.tile_span;
+    span8 = t;
+    span16 = std::min(span16, t);
+    span32 = std::min(span32, t);
+    use_table = false;
   }
-  int blocks = opts.blocks > 0 ? opts.blocks : g.num_sms;
+  int blocks = opts.blocks > 0 ? opts.blocks : g.num_sms * L.blocks_per_sm;
   if (blocks > g.block_work_cap) {
     cudaFree(g.block_work);
     g.block_work = nullptr;
@@ -378,21 +600,27 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     g.block_work_cap = blocks;
   }
   const uint32_t n = (uint32_t)g.n;
-  const uint32_t ntasks = n > (uint32_t)opts.part_index ? (n - (uint32_t)opts.part_index + part_count - 1) / part_count : 0u;
+  const uint32_t ntasks =
+      n > (uint32_t)opts.part_index ? (n - (uint32_t)opts.part_index + part_count - 1) / part_count : 0u;
 
   Params P;
   P.adj = g.adj;
   P.rec = g.rec;
+  P.coff = g.coff;
   P.aoff = g.aoff;
   P.awork = g.awork;
   P.order = g.order;
+  P.bnd = use_table ? g.bnd : nullptr;
+  P.nbands = g.nbands;
   P.n = n;
   P.ntasks = ntasks;
   P.part_index = (uint32_t)opts.part_index;
   P.part_count = (uint32_t)part_count;
+  P.span8 = span8;
   P.span16 = span16;
   P.span32 = span32;
-  P.cap_words = (uint32_t)cap_words;
+  P.cap_words = (uint32_t)L.cap_words;
+  P.fast = (opts.flags & 1) ? 0 : 1;
   P.dynamic = opts.algo == BBC_ALGO_GBBCPP;
   P.acc = g.acc;
   P.queue = g.queue;
@@ -401,7 +629,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
   BBC_CK(cudaMemsetAsync(g.acc, 0, 32, g.stream));
   BBC_CK(cudaMemsetAsync(g.queue, 0, 4, g.stream));
   BBC_CK(cudaEventRecord(g.ev0, g.stream));
-  k_count<<<blocks, kCountThreads, smem_bytes, g.stream>>>(P);
+  L.kernel<<<blocks, L.threads, L.smem_bytes, g.stream>>>(P);
   BBC_CK(cudaGetLastError());
   BBC_CK(cudaEventRecord(g.ev1, g.stream));
   unsigned long long h_acc[4];
@@ -426,7 +654,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     st->unbalanced_hi = h_acc[3];
     st->anchor_side = g.side;
     st->blocks = blocks;
-    st->threads = kCountThreads;
+    st->threads = L.threads;
     st->tile_span = (int32_t)span16;
     st->tasks = (int32_t)ntasks;
     st->preprocess_ms = g.preprocess_ms;

@@ -16,8 +16,10 @@ namespace bbc {
 //                    word = rank(w) | neg(c, w) << 31  (sign packed in bit 31)
 //  coff  u32[nc + 1] centre offsets into adj
 //  rec   uint2[m]    one record per anchor-side edge (a, c), grouped by rank(a):
-//                    x = begin | neg(a, c) << 31, y = end; [begin, end) is the
+//                    x = begin | neg(a, c) << 31, y = c; [begin, coff[c+1]) is the
 //                    admitted suffix of c's list (ranks > rank(a))
+//  bnd   u32[nc * nbands] (optional) band table: bnd[c * nbands + j] = first position
+//                    of c's list with rank >= n - j * t16 (j = 0: list end)
 //  aoff  u32[n + 1]  anchor offsets into rec (by rank)
 //  awork u64[n]      admitted wedges per anchor (= sum of end - begin)
 //  order u32[n]      anchor ranks by descending awork (G-BBC++ dispatch order)
@@ -38,6 +40,9 @@ struct Graph {
   unsigned long long* awork = nullptr;
   uint32_t* order = nullptr;
   uint32_t* rank_to_id = nullptr;
+  uint32_t* bnd = nullptr;
+  uint32_t nbands = 0;
+  uint32_t t16 = 0;
   // count scratch
   unsigned long long* acc = nullptr;        // [4]: bal lo, bal hi, unb lo, unb hi
   unsigned int* queue = nullptr;            // [1]
@@ -46,11 +51,13 @@ struct Graph {
   int last_blocks = 0;
   int num_sms = 0;
   int max_smem = 0;
+  int threads = 256;  // count-kernel CTA size (128 / 256 / 512 / 1024; env BBC_THREADS)
   float preprocess_ms = 0.f;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
 void set_error(const std::string& msg, int64_t info = 0);
+int count_span16(Graph& g);  // endpoint span of a packed u16x2 tile on g.device
 int cuda_fail(cudaError_t e, const char* where);
 
 #define BBC_CK(call)                                              \

@@ -15,6 +15,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "bbc_internal.cuh"
@@ -128,20 +130,47 @@ __global__ void k_adj_dup(const unsigned long long* __restrict__ keys, int64_t m
   }
 }
 
-// records in anchor-rank order: rec[j] = {(i + 1) | neg << 31, coff[c + 1]}
+// records in anchor-rank order: rec[j] = {(i + 1) | neg << 31, c}; the admitted suffix of
+// centre c's list is [i + 1, coff[c + 1])
 __global__ void k_records(const uint32_t* __restrict__ pos_sorted, const unsigned long long* __restrict__ keys,
-                          const uint32_t* __restrict__ coff, int64_t m, uint2* __restrict__ rec) {
+                          int64_t m, uint2* __restrict__ rec) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
     uint32_t i = pos_sorted[j];
     unsigned long long k = keys[i];
-    uint32_t c = (uint32_t)(k >> 32);
-    rec[j] = make_uint2((i + 1u) | ((uint32_t)(k & 1ull) << 31), coff[c + 1]);
+    rec[j] = make_uint2((i + 1u) | ((uint32_t)(k & 1ull) << 31), (uint32_t)(k >> 32));
+  }
+}
+
+// band table: row c holds, for j in [0, nbands), the first position of c's list whose
+// rank is >= n - j * t (j = 0: the list end).  Lists are rank-sorted.
+__global__ void k_band_table(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ coff, int64_t nc,
+                             uint32_t nbands, uint32_t t, uint32_t n, uint32_t* __restrict__ bnd) {
+  const int64_t total = nc * (int64_t)nbands;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / nbands;
+    const uint32_t j = (uint32_t)(e - c * nbands);
+    uint32_t lo = coff[c], hi = coff[c + 1];
+    if (j > 0) {
+      const int64_t x = (int64_t)n - (int64_t)j * t;
+      if (x <= 0) {
+        hi = lo;
+      } else {
+        while (lo < hi) {
+          uint32_t mid = (lo + hi) >> 1;
+          if ((int64_t)(adj[mid] & 0x7fffffffu) < x)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+      }
+    }
+    bnd[e] = hi;
   }
 }
 
 // admitted wedges per anchor: one warp per anchor
-__global__ void k_anchor_work(const uint2* __restrict__ rec, const uint32_t* __restrict__ aoff, int64_t n,
-                              unsigned long long* __restrict__ awork) {
+__global__ void k_anchor_work(const uint2* __restrict__ rec, const uint32_t* __restrict__ aoff,
+                              const uint32_t* __restrict__ coff, int64_t n, unsigned long long* __restrict__ awork) {
   int lane = threadIdx.x & 31;
   int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -149,7 +178,7 @@ __global__ void k_anchor_work(const uint2* __restrict__ rec, const uint32_t* __r
     unsigned long long acc = 0;
     for (uint32_t e = aoff[a] + lane; e < aoff[a + 1]; e += 32) {
       uint2 r = rec[e];
-      acc += r.y - (r.x & 0x7fffffffu);
+      acc += coff[r.y + 1] - (r.x & 0x7fffffffu);
     }
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) awork[a] = acc;
@@ -195,6 +224,8 @@ void free_graph_arrays(Graph& g) {
   cudaFree(g.acc);
   cudaFree(g.queue);
   cudaFree(g.block_work);
+  cudaFree(g.bnd);
+  g.bnd = nullptr;
   g.adj = g.coff = g.aoff = g.order = g.rank_to_id = nullptr;
   g.rec = nullptr;
   g.awork = g.acc = g.block_work = nullptr;
@@ -344,8 +375,7 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
     tb = t6;
     BBC_CK(cub::DeviceRadixSort::SortPairs(temp.p, tb, akey_a.as<uint32_t>(), akey_b.as<uint32_t>(),
                                            aval_a.as<uint32_t>(), aval_b.as<uint32_t>(), (int)m, 0, rank_bits, st));
-    k_records<<<grid_for(m, sms), kThreads, 0, st>>>(aval_b.as<uint32_t>(), keys_b.as<unsigned long long>(), g.coff, m,
-                                                     g.rec);
+    k_records<<<grid_for(m, sms), kThreads, 0, st>>>(aval_b.as<uint32_t>(), keys_b.as<unsigned long long>(), m, g.rec);
   }
   // anchor offsets from degrees in rank order
   if (n > 0) {
@@ -358,7 +388,7 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
 
   // ---- K5: per-anchor work and the G-BBC++ dispatch order ---------------------------------
   if (n > 0) {
-    k_anchor_work<<<grid_for(n * 32, sms), kThreads, 0, st>>>(g.rec, g.aoff, n, g.awork);
+    k_anchor_work<<<grid_for(n * 32, sms), kThreads, 0, st>>>(g.rec, g.aoff, g.coff, n, g.awork);
     k_iota<<<grid_for(n, sms), kThreads, 0, st>>>(ids.as<uint32_t>(), n);
     // descending work; LSD radix descending sort is stable -> ties in ascending rank
     unsigned long long* work_sorted = keys_a.as<unsigned long long>();
@@ -367,6 +397,24 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
                                                      (int)n, 0, 64, st));
   }
   BBC_CK(cudaGetLastError());
+
+  // band table: only when it fits a modest memory budget
+  {
+    int span16 = count_span16(g);
+    if (span16 <= 0) return BBC_ERR_CUDA;
+    g.t16 = (uint32_t)span16;
+    g.nbands = (uint32_t)((n + span16 - 1) / span16);
+    if (g.nbands == 0) g.nbands = 1;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t need = (size_t)nc * g.nbands * 4;
+    if (nc > 0 && n > 0 && need <= std::min<size_t>((size_t)8 << 30, free_b / 4)) {
+      BBC_ALLOC(g.bnd, need);
+      k_band_table<<<grid_for(nc * (int64_t)g.nbands, sms), kThreads, 0, st>>>(g.adj, g.coff, nc, g.nbands, g.t16,
+                                                                                 (uint32_t)n, g.bnd);
+      BBC_CK(cudaGetLastError());
+    }
+  }
 
   BBC_ALLOC(g.acc, 64);
   BBC_ALLOC(g.queue, 64);
@@ -398,6 +446,10 @@ int init_handle(Graph& g, int device, int64_t n_u, int64_t n_v, int64_t m) {
   g.m = m;
   BBC_CK(cudaDeviceGetAttribute(&g.num_sms, cudaDevAttrMultiProcessorCount, device));
   BBC_CK(cudaDeviceGetAttribute(&g.max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  if (const char* e = std::getenv("BBC_THREADS")) {
+    int t = std::atoi(e);
+    if (t == 128 || t == 256 || t == 512 || t == 1024) g.threads = t;
+  }
   BBC_CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
   BBC_CK(cudaEventCreate(&g.ev0));
   BBC_CK(cudaEventCreate(&g.ev1));

@@ -71,9 +71,10 @@ def test_synthetic_configs_vs_reference(gpu, golden, key):
     for side in (SIDE_CHEAPER, SIDE_U, SIDE_V):
         for algo in ALGOS:
             g = DeviceGraph.from_host(cfg.n_u, cfg.n_v, u, v, s, 0, side)
-            r = g.count(algo)
-            assert (r.balanced, r.unbalanced) == (rec["balanced"], rec["unbalanced"]), (key, side, algo)
-            assert r.wedges == r.wedges_total == (rec["w_u"] if g.anchor_side == 0 else rec["w_v"])
+            for flags in (0, _lib.FLAG_BANDED_ONLY):
+                r = g.count(algo, flags=flags)
+                assert (r.balanced, r.unbalanced) == (rec["balanced"], rec["unbalanced"]), (key, side, algo, flags)
+                assert r.wedges == r.wedges_total == (rec["w_u"] if g.anchor_side == 0 else rec["w_v"])
             assert (g.w_u, g.w_v) == (rec["w_u"], rec["w_v"])
             g.close()
 
