@@ -38,7 +38,7 @@ L2_FLUSH_BYTES = 512 << 20
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", type=int, default=2)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
@@ -79,7 +79,7 @@ class ClockSampler:
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.QUERY}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.fh,
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -279,12 +279,13 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     n_s = g.n_anchors
     alg_bytes = 4 * w_s + 12 * m + 8 * n_s
-    achieved = alg_bytes / (count_ms_local * 1e-3) / 1e9 / world if world > 1 else alg_bytes / (count_ms_local * 1e-3) / 1e9
-    traffic = None
-    prof = ROOT / "profiles" / "count_kernel_traffic.json"
-    if prof.exists():
+    achieved = alg_bytes / world / (count_ms_local * 1e-3) / 1e9  # per GPU: each counts ~1/world of the wedges
+    traffic, traffic_src = None, None
+    profs = sorted((ROOT / "profiles").glob(f"r*_k_count_config{args.config}.json"))
+    if profs:  # dram__bytes_read.sum + dram__bytes_write.sum of the latest committed ncu capture
         try:
-            traffic = json.loads(prof.read_text()).get(cfg.name)
+            traffic = json.loads(profs[-1].read_text()).get("traffic_bytes")
+            traffic_src = f"profiles/{profs[-1].name}"
         except Exception:
             traffic = None
 
@@ -306,7 +307,7 @@ def main():
                 "d2h_bytes_per_step": 64 + 8 + 32 + 8 * r.blocks, "end_to_end_count_ms": e2e_s * 1e3,
                 "gpu_launches_per_step": e2e_launch, "path": "bbc_graph_create(host arrays) + bbc_count"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "algorithmic_bytes": alg_bytes,
+                     "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes": alg_bytes,
                      "bytes_model": "4*W_S + 12*|E| + 8*|S| (BASELINE.md 2)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650"},
         "clocks": clocks.summary(),
