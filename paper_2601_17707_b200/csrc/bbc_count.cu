@@ -57,6 +57,13 @@ struct Params {
   uint32_t span32;
   uint32_t cap_words;
   int fast;         // 0: always the general banded path (flags bit 0)
+  uint32_t hslots;  // cold-range hash slots (0: band by band; flags bit 1)
+  uint32_t t16;     // band-table granularity (ranks per column)
+  uint32_t bcols8;  // this launch's tile band in table columns (W8 / W16 layouts)
+  uint32_t bcols16;
+  int phase;        // 0: every band; 1: hub band only; 2: cold range only
+  uint32_t fast_max;  // largest degree on the fast path (same for every launch of a count)
+  int debug;        // flags bits 2 / 3: skip band 0 / skip the cold range (timing only)
   int dynamic;
   unsigned long long* acc;
   unsigned int* queue;
@@ -168,6 +175,80 @@ __device__ __forceinline__ void walk(const Params& P, uint32_t* cnt, const uint3
                                      const uint32_t* s_pfx, int nb, uint32_t ngroups, uint32_t lo_rank,
                                      unsigned long long& tb, unsigned long long& tu) {
   const uint4* adj4 = reinterpret_cast<const uint4*>(P.adj);
+  // two groups per thread per iteration, both loads in flight before either is used
+  for (uint32_t g0 = threadIdx.x; g0 < ngroups; g0 += 2 * T) {
+    uint4 q[2];
+    uint32_t lo[2], hi[2], sg[2], p0[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint32_t g = g0 + (uint32_t)i * T;
+      lo[i] = 1u;
+      hi[i] = 0u;
+      sg[i] = 0u;
+      p0[i] = 0u;
+      q[i] = make_uint4(0u, 0u, 0u, 0u);
+      if (g < ngroups) {
+        const int k = find_record(s_pfx, nb, g);
+        const uint32_t lox = s_lo[k];
+        lo[i] = lox & 0x7fffffffu;
+        sg[i] = lox & 0x80000000u;
+        hi[i] = s_hi[k];
+        const uint32_t grp = (lo[i] >> 2) + (g - s_pfx[k]);
+        p0[i] = grp << 2;
+        q[i] = ld_stream(adj4 + grp);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint32_t wv[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t p = p0[i] + (uint32_t)j;
+        if (p >= lo[i] && p < hi[i]) {
+          const uint32_t word = wv[j];
+          const uint32_t rel = (word & 0x7fffffffu) - lo_rank;
+          const uint32_t par = (word ^ sg[i]) >> 31;  // 1: asymmetric (negative) wedge
+          if (M == kDense) {
+            bump<W>(cnt, rel, par);
+          } else if (M == kSparse) {
+            bump_close<W>(cnt, rel, par, tb, tu);
+          } else {
+            cnt[W == 8 ? (rel >> 1) : rel] = 0u;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Cold-range accumulation in a shared-memory hash table: slot i holds key = rank + 1
+// (0 = empty) in word 2i and the packed u16 positive | negative counts in word 2i + 1;
+// linear probing over K slots; closing inline from the add's return value.
+__device__ __forceinline__ void hash_bump_close(uint32_t* tab, uint32_t K, uint32_t rank, uint32_t par,
+                                                unsigned long long& tb, unsigned long long& tu) {
+  const uint32_t key = rank + 1u;
+  uint32_t h = (uint32_t)(((unsigned long long)(key * 0x9E3779B1u) * K) >> 32);
+  volatile uint32_t* vk = tab;
+  for (;;) {
+    uint32_t k = vk[2u * h];
+    if (k == key) break;
+    if (k == 0u) {
+      k = atomicCAS(&tab[2u * h], 0u, key);
+      if (k == 0u || k == key) break;
+    }
+    h = (h + 1u == K) ? 0u : h + 1u;
+  }
+  const uint32_t sh = par << 4;
+  const uint32_t old = atomicAdd(&tab[2u * h + 1u], 1u << sh);
+  tb += (old >> sh) & 0xffffu;
+  tu += (old >> (sh ^ 16u)) & 0xffffu;
+}
+
+template <int T>
+__device__ __forceinline__ void walk_hash(const Params& P, uint32_t* tab, uint32_t K, const uint32_t* s_lo,
+                                          const uint32_t* s_hi, const uint32_t* s_pfx, int nb, uint32_t ngroups,
+                                          unsigned long long& tb, unsigned long long& tu) {
+  const uint4* adj4 = reinterpret_cast<const uint4*>(P.adj);
   for (uint32_t g = threadIdx.x; g < ngroups; g += T) {
     const int k = find_record(s_pfx, nb, g);
     const uint32_t lox = s_lo[k];
@@ -179,18 +260,7 @@ __device__ __forceinline__ void walk(const Params& P, uint32_t* cnt, const uint3
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t p = p0 + (uint32_t)j;
-      if (p >= lo && p < hi) {
-        const uint32_t word = wv[j];
-        const uint32_t rel = (word & 0x7fffffffu) - lo_rank;
-        const uint32_t par = (word ^ sgn) >> 31;  // 1: asymmetric (negative) wedge
-        if (M == kDense) {
-          bump<W>(cnt, rel, par);
-        } else if (M == kSparse) {
-          bump_close<W>(cnt, rel, par, tb, tu);
-        } else {
-          cnt[W == 8 ? (rel >> 1) : rel] = 0u;
-        }
-      }
+      if (p >= lo && p < hi) hash_bump_close(tab, K, wv[j] & 0x7fffffffu, (wv[j] ^ sgn) >> 31, tb, tu);
     }
   }
 }
@@ -358,39 +428,46 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
   }
 }
 
-// Anchors with deg <= T and a band table (layouts W8 / W16): the records stay in
-// registers for all bands, each band's lower table column is prefetched one band ahead,
-// sparse bands close inline (zeroing from registers when <= 2 groups per thread, else
-// by a re-walk), dense bands use a no-return increment and a closing sweep.
+// Anchors with deg <= T and a band table (layouts W8 / W16).  Work is done in rounds;
+// a round covers a range of table columns [ca, cb) = end-vertex ranks
+// [n - cb * t16, n - ca * t16) and walks every record's sub-slice of that range once:
+//   * the hub band (the top `hstep` columns: the high-degree end vertices that receive
+//     most wedges) is a tile round (phase 1);
+//   * the colder columns (phase 2) go through the hash table in one round when they fit
+//     at load <= 2/3, else one tile round per band of `bstep` columns.
+// Phase 0 runs both in one launch.  Tile rounds with <= 2 groups per thread close inline
+// and zero from registers; larger ones use no-return increments and the closing sweep.
+// Records stay in registers across rounds.
 template <int T, int W>
 __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, uint32_t rb, uint32_t re,
                                     unsigned long long& tb, unsigned long long& tu, unsigned long long& work) {
-  const uint32_t span = W == 8 ? P.span8 : P.span16;
-  const uint32_t step = W == 8 ? 2u : 1u;
-  const uint32_t nbu = (P.n - 1u - r) / span + 1u;
+  const uint32_t step = W == 8 ? P.bcols8 : P.bcols16;     // this launch's tile band: columns
+  // hub band: the phase-1 tile (128 x 8 configuration = table granularity), or this
+  // launch's tile when one launch does every band
+  const uint32_t hstep = P.phase == 0 ? step : (W == 8 ? 2u : 1u);
+  const uint32_t t16 = P.t16;
+  const uint32_t ncols = min(P.nbands, (P.n - 1u - r) / t16 + 1u);  // columns holding ranks > r
   const int nb = (int)(re - rb);
   const bool mine = (int)threadIdx.x < nb;
-  uint32_t recx = 0u, hi_next = 0u, lo_next = 0u;
+  uint32_t recx = 0u;
   const uint32_t* row = P.bnd;
   if (mine) {
     const uint2 rr = P.rec[rb + threadIdx.x];
     recx = rr.x;
     row = P.bnd + (size_t)rr.y * P.nbands;
-    hi_next = __ldg(row);
-    lo_next = step < P.nbands ? __ldg(row + step) : 0u;
   }
-  for (uint32_t b = 0; b < nbu; ++b) {
-    const long long top = (long long)P.n - (long long)b * span;
-    const long long bot = top - (long long)span;
-    const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
-    const uint32_t band_span = (uint32_t)(top - (long long)lo_rank);
+  // table column j of this thread's record (0 past the last column: start of the list)
+  auto col = [&](uint32_t j) -> uint32_t { return (mine && j < P.nbands) ? __ldg(row + j) : 0u; };
+  // columns needed up front are loaded together (one latency)
+  const uint32_t c0 = P.phase == 2 ? 0u : col(0u), c1 = col(hstep);
+  const uint32_t c2 = P.phase == 1 ? 0u : col(min(hstep + step, ncols));
+  const uint32_t cn = P.phase == 1 ? 0u : col(ncols);
+  // sub-slices [lo, hi) (positions of two table columns) -> S arrays, block scan;
+  // returns total groups, bw = total wedges
+  auto setup = [&](uint32_t hi, uint32_t lo, unsigned long long& bw) -> uint32_t {
     uint32_t ng = 0;
     unsigned long long myw = 0;
     if (mine) {
-      uint32_t hi = hi_next, lo = lo_next;
-      const uint32_t j2 = (b + 2u) * step;
-      hi_next = lo;
-      lo_next = (b + 1u < nbu && j2 < P.nbands) ? __ldg(row + j2) : 0u;  // prefetch for band b + 1
       lo = max(lo, recx & 0x7fffffffu);
       hi = max(hi, lo);
       if (hi > lo) {
@@ -401,12 +478,17 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       S.hi[threadIdx.x] = hi;
     }
     uint32_t ngroups;
-    unsigned long long bw;
     const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w);
     if (mine) S.pfx[threadIdx.x] = ex;
     __syncthreads();
-    work += myw;
-    if (ngroups == 0) continue;
+    return ngroups;
+  };
+  // one tile round over band columns [ca, ca + cols)
+  auto tile_round = [&](uint32_t ca, uint32_t cols, uint32_t ngroups, unsigned long long bw) {
+    const long long top = (long long)P.n - (long long)ca * t16;
+    const long long bot = top - (long long)cols * t16;
+    const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
+    const uint32_t band_span = (uint32_t)(top - (long long)lo_rank);
     const uint32_t band_words = W == 8 ? (band_span + 1u) / 2u : band_span;
     if (ngroups <= 2u * T) {
       uint32_t touched[8];
@@ -415,23 +497,68 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (touched[j] != 0xffffffffu) S.cnt[touched[j]] = 0u;
-      __syncthreads();
-    } else if (bw < band_words) {
+    } else if (P.debug & 16) {  // (A/B switch) inline closing + global re-walk to zero
       walk<T, W, kSparse>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
       __syncthreads();
       walk<T, W, kZero>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
-      __syncthreads();
     } else {
+      // more than two groups per thread: no-return increments and the shared-memory
+      // closing sweep, which is cheaper than re-reading the adjacency to zero
       walk<T, W, kDense>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
       __syncthreads();
       sweep<T, W>(S.cnt, band_words, tb, tu);
-      __syncthreads();
+    }
+    __syncthreads();
+  };
+  auto hash_round = [&](uint32_t ngroups, unsigned long long bw) {
+    const uint32_t K = min(P.hslots, max(64u, (uint32_t)(2ull * bw + 31ull) & ~31u));
+    walk_hash<T>(P, S.cnt, K, S.lo, S.hi, S.pfx, nb, ngroups, tb, tu);
+    __syncthreads();
+    uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
+    for (uint32_t i = threadIdx.x; i < (2u * K + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+  };
+  // band-by-band tile rounds over columns [ca, cb); a band is `step` columns starting at
+  // any column (the table has every boundary), the last one truncated at cb
+  // (work is a per-thread partial summed over the CTA at the end: thread 0 adds totals)
+  const bool t0 = threadIdx.x == 0;
+  // tiles over columns [step, ncols): the column values are carried from band to band and
+  // the next band's lower column is prefetched while the current band runs
+  auto tiles = [&]() {
+    uint32_t hi = c1, lo = c2;
+    for (uint32_t c = hstep; c < ncols; c += step) {
+      const uint32_t nxt = c + step < ncols ? col(min(c + 2u * step, ncols)) : 0u;
+      unsigned long long bw;
+      const uint32_t ng = setup(hi, lo, bw);
+      if (t0) work += bw;
+      if (ng) tile_round(c, step, ng, bw);
+      hi = lo;
+      lo = nxt;
+    }
+  };
+
+  // the hub band
+  if (P.phase != 2 && !(P.debug & 4)) {
+    unsigned long long bw;
+    const uint32_t ng = setup(c0, c1, bw);
+    if (t0) work += bw;
+    if (ng) tile_round(0u, hstep, ng, bw);
+  }
+  if (P.phase == 1 || ncols <= hstep || (P.debug & 8)) return;
+  if (P.hslots != 0u) {
+    unsigned long long wc;
+    const uint32_t ng = setup(c1, cn, wc);
+    if (3ull * wc <= 2ull * P.hslots) {  // the whole cold range in one hash round (load <= 2/3)
+      if (t0) work += wc;
+      if (ng) hash_round(ng, wc);
+      return;
     }
   }
+  tiles();
 }
 
-template <int T>
-__global__ void __launch_bounds__(T, 1024 / T) k_count(Params P) {
+template <int T, int MINB>
+__global__ void __launch_bounds__(T, MINB) k_count(Params P) {
   constexpr int kWarps = T / 32;
   extern __shared__ uint4 smem4[];
   __shared__ uint32_t s_v[32];
@@ -468,7 +595,13 @@ __global__ void __launch_bounds__(T, 1024 / T) k_count(Params P) {
     const uint32_t rb = P.aoff[r], re = P.aoff[r + 1];
     const uint32_t deg = re - rb;
     unsigned long long tb = 0, tu = 0;
-    const bool fast = P.fast && P.bnd != nullptr && deg <= (uint32_t)T;
+    // fast path: every record held by one thread; the bound is the same for all launches of
+    // a count so that phases agree on which anchors they split
+    const bool fast = P.fast && P.bnd != nullptr && deg <= min((uint32_t)T, P.fast_max);
+    if (!fast && P.phase == 2) {  // general-path anchors are done entirely in phase 1
+      __syncthreads();
+      continue;
+    }
     if (fast && deg <= 255u)
       process_anchor_fast<T, 8>(P, S, r, rb, re, tb, tu, work);
     else if (fast)
@@ -508,7 +641,7 @@ __global__ void __launch_bounds__(T, 1024 / T) k_count(Params P) {
   if (threadIdx.x == 0) {
     unsigned long long t = 0;
     for (int w = 0; w < kWarps; ++w) t += s_w[w];
-    P.block_work[blockIdx.x] = t;
+    P.block_work[blockIdx.x] += t;  // launches of one count accumulate (zeroed per count)
   }
 }
 
@@ -520,44 +653,49 @@ struct Launch {
   void (*kernel)(Params) = nullptr;
 };
 
-template <int T>
+// T threads per CTA, MINB CTAs per SM: shared memory is split evenly between the CTAs of
+// an SM (1 KB per CTA is reserved by the driver) and registers are capped accordingly.
+template <int T, int MINB>
 int configure_t(Graph& g, Launch& L) {
   cudaFuncAttributes fa;
-  BBC_CK(cudaFuncGetAttributes(&fa, k_count<T>));
+  BBC_CK(cudaFuncGetAttributes(&fa, k_count<T, MINB>));
   int per_sm = 0;
   BBC_CK(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, g.device));
-  const int bps = 1024 / T;
-  // per-CTA budget: an equal share of the SM (1 KB per CTA is reserved by the driver)
-  int budget = std::min(g.max_smem, per_sm / bps - 1024);
+  int budget = std::min(g.max_smem, per_sm / MINB - 1024);
   int avail = budget - (int)fa.sharedSizeBytes - (3 * T * 4 + 64);
   L.threads = T;
-  L.blocks_per_sm = bps;
+  L.blocks_per_sm = MINB;
   L.cap_words = (avail / 16) * 4;
   L.smem_bytes = L.cap_words * 4 + 3 * T * 4 + 16;
-  L.kernel = k_count<T>;
-  BBC_CK(cudaFuncSetAttribute(k_count<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes));
+  L.kernel = k_count<T, MINB>;
+  BBC_CK(cudaFuncSetAttribute(k_count<T, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes));
   return BBC_OK;
 }
 
+// single-launch configuration (all phases): BBC_THREADS, default 128 x 8 per SM
 int configure(Graph& g, Launch& L) {
   switch (g.threads) {
-    case 128:
-      return configure_t<128>(g, L);
     case 256:
-      return configure_t<256>(g, L);
+      return configure_t<256, 4>(g, L);
     case 512:
-      return configure_t<512>(g, L);
+      return configure_t<512, 2>(g, L);
+    case 1024:
+      return configure_t<1024, 1>(g, L);
     default:
-      return configure_t<1024>(g, L);
+      return configure_t<128, 8>(g, L);
   }
 }
 
+// two-phase configuration: hub band with 128 x 8, cold range with 256 x 2 (big hash)
+int configure_cold(Graph& g, Launch& L) { return configure_t<256, 2>(g, L); }
+
 }  // namespace
 
+// Table granularity: the W16 span of the 128 x 8 configuration (hub band of phase 1).
 int count_span16(Graph& g) {
   Launch L;
   BBC_CK(cudaSetDevice(g.device));
-  if (configure(g, L)) return -1;
+  if (configure_t<128, 8>(g, L)) return -1;
   return L.cap_words - 8;
 }
 
@@ -578,21 +716,22 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     return BBC_ERR_ARG;
   }
   BBC_CK(cudaSetDevice(g.device));
-  Launch L;
+  Launch L, Lc;
   int rc = configure(g, L);
   if (rc) return rc;
-  uint32_t span16 = (uint32_t)L.cap_words - 8u;
-  uint32_t span8 = 2u * span16, span32 = span16 / 2u;
-  bool use_table = g.bnd != nullptr && span16 == g.t16;
-  if (opts.tile_span > 0 && (uint32_t)opts.tile_span < span8) {
-    // TileConfig.tile_size: bands of at most tile_span end vertices in every layout
-    const uint32_t t = (uint32_t)opts.tile_span;
-    span8 = t;
-    span16 = std::min(span16, t);
-    span32 = std::min(span32, t);
-    use_table = false;
+  bool use_table = g.bnd != nullptr;
+  const bool tile_override = opts.tile_span > 0 && (uint32_t)opts.tile_span < 2u * ((uint32_t)L.cap_words - 8u);
+  if (tile_override) use_table = false;
+  // flags bit 6 (experimental, measured slower on config 2): hub band and cold range in
+  // two launches with different CTA shapes
+  const bool two_phase = use_table && (opts.flags & 64) && (opts.flags & 1) == 0;
+  if (two_phase) {
+    rc = configure_cold(g, Lc);
+    if (rc) return rc;
   }
-  int blocks = opts.blocks > 0 ? opts.blocks : g.num_sms * L.blocks_per_sm;
+  const int blocks1 = opts.blocks > 0 ? opts.blocks : g.num_sms * L.blocks_per_sm;
+  const int blocks2 = two_phase ? (opts.blocks > 0 ? opts.blocks : g.num_sms * Lc.blocks_per_sm) : 0;
+  const int blocks = std::max(blocks1, blocks2);
   if (blocks > g.block_work_cap) {
     cudaFree(g.block_work);
     g.block_work = nullptr;
@@ -603,35 +742,62 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
   const uint32_t ntasks =
       n > (uint32_t)opts.part_index ? (n - (uint32_t)opts.part_index + part_count - 1) / part_count : 0u;
 
-  Params P;
-  P.adj = g.adj;
-  P.rec = g.rec;
-  P.coff = g.coff;
-  P.aoff = g.aoff;
-  P.awork = g.awork;
-  P.order = g.order;
-  P.bnd = use_table ? g.bnd : nullptr;
-  P.nbands = g.nbands;
-  P.n = n;
-  P.ntasks = ntasks;
-  P.part_index = (uint32_t)opts.part_index;
-  P.part_count = (uint32_t)part_count;
-  P.span8 = span8;
-  P.span16 = span16;
-  P.span32 = span32;
-  P.cap_words = (uint32_t)L.cap_words;
-  P.fast = (opts.flags & 1) ? 0 : 1;
-  P.dynamic = opts.algo == BBC_ALGO_GBBCPP;
-  P.acc = g.acc;
-  P.queue = g.queue;
-  P.block_work = g.block_work;
+  auto params = [&](const Launch& X, int phase) {
+    Params P;
+    uint32_t span16 = (uint32_t)X.cap_words - 8u;
+    uint32_t span8 = 2u * span16, span32 = span16 / 2u;
+    if (tile_override) {
+      // TileConfig.tile_size: bands of at most tile_span end vertices in every layout
+      const uint32_t t = (uint32_t)opts.tile_span;
+      span8 = t;
+      span16 = std::min(span16, t);
+      span32 = std::min(span32, t);
+    }
+    P.adj = g.adj;
+    P.rec = g.rec;
+    P.coff = g.coff;
+    P.aoff = g.aoff;
+    P.awork = g.awork;
+    P.order = g.order;
+    P.bnd = use_table ? g.bnd : nullptr;
+    P.nbands = g.nbands;
+    P.t16 = g.t16;
+    P.bcols16 = std::max(1u, span16 / std::max(1u, g.t16));
+    P.bcols8 = std::max(2u, span8 / std::max(1u, g.t16));
+    P.phase = phase;
+    P.n = n;
+    P.ntasks = ntasks;
+    P.part_index = (uint32_t)opts.part_index;
+    P.part_count = (uint32_t)part_count;
+    P.span8 = span8;
+    P.span16 = span16;
+    P.span32 = span32;
+    P.cap_words = (uint32_t)X.cap_words;
+    P.fast = (opts.flags & 1) ? 0 : 1;
+    P.fast_max = two_phase ? (uint32_t)std::min(L.threads, Lc.threads) : (uint32_t)X.threads;
+    P.hslots = (opts.flags & 2) ? 0u : (uint32_t)X.cap_words / 2u;
+    P.debug = opts.flags;
+    P.dynamic = opts.algo == BBC_ALGO_GBBCPP;
+    P.acc = g.acc;
+    P.queue = g.queue + (phase == 2 ? 1 : 0);
+    P.block_work = g.block_work;
+    return P;
+  };
 
   BBC_CK(cudaMemsetAsync(g.acc, 0, 32, g.stream));
-  BBC_CK(cudaMemsetAsync(g.queue, 0, 4, g.stream));
+  BBC_CK(cudaMemsetAsync(g.queue, 0, 8, g.stream));
+  BBC_CK(cudaMemsetAsync(g.block_work, 0, (size_t)blocks * 8, g.stream));
   BBC_CK(cudaEventRecord(g.ev0, g.stream));
-  L.kernel<<<blocks, L.threads, L.smem_bytes, g.stream>>>(P);
+  const Params P1 = params(L, two_phase ? 1 : 0);
+  L.kernel<<<blocks1, L.threads, L.smem_bytes, g.stream>>>(P1);
   BBC_CK(cudaGetLastError());
+  if (two_phase) {
+    const Params P2 = params(Lc, 2);
+    Lc.kernel<<<blocks2, Lc.threads, Lc.smem_bytes, g.stream>>>(P2);
+    BBC_CK(cudaGetLastError());
+  }
   BBC_CK(cudaEventRecord(g.ev1, g.stream));
+  const uint32_t span16 = P1.span16;
   unsigned long long h_acc[4];
   BBC_CK(cudaMemcpyAsync(h_acc, g.acc, 32, cudaMemcpyDeviceToHost, g.stream));
   BBC_CK(cudaStreamSynchronize(g.stream));

@@ -51,7 +51,7 @@ struct Graph {
   int last_blocks = 0;
   int num_sms = 0;
   int max_smem = 0;
-  int threads = 256;  // count-kernel CTA size (128 / 256 / 512 / 1024; env BBC_THREADS)
+  int threads = 128;  // count-kernel CTA size (128 / 256 / 512 / 1024; env BBC_THREADS)
   float preprocess_ms = 0.f;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
