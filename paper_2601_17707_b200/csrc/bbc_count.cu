@@ -62,6 +62,9 @@ struct Params {
   uint32_t bcols8;  // this launch's tile band in table columns (W8 / W16 layouts)
   uint32_t bcols16;
   int phase;        // 0: every band; 1: hub band only; 2: cold range only
+  uint32_t bm_cols;    // cold seen-bitmap round width in table columns (0: off)
+  uint32_t bm_words;   // bitmap words (start of the repeat set)
+  uint32_t rep_slots;  // repeat-set slots (keys, then packed counts)
   uint32_t fast_max;  // largest degree on the fast path (same for every launch of a count)
   int debug;        // flags bits 2 / 3: skip band 0 / skip the cold range (timing only)
   int dynamic;
@@ -265,6 +268,104 @@ __device__ __forceinline__ void walk_hash(const Params& P, uint32_t* tab, uint32
   }
 }
 
+// ---- cold bands: seen-bitmap + repeat set ---------------------------------------------
+// In the cold end-vertex range almost every (anchor, end vertex) pair has one common
+// centre, and a pair with one wedge contributes nothing.  A cold round therefore walks
+// its wedges twice: pass A sets one bit per end vertex (16x denser than a u8x2 counter,
+// so one round spans 16x more ranks) and inserts an end vertex into a small hash set
+// when its bit was already set; pass B counts exactly, in that set, every wedge whose end
+// vertex repeats, closing inline from the add's return value.  If the set would exceed
+// half its slots the round falls back to counter tiles.
+__device__ __forceinline__ uint32_t rep_hash(uint32_t key, uint32_t K) {
+  return (uint32_t)(((unsigned long long)(key * 0x9E3779B1u) * K) >> 32);
+}
+
+// insert key (rank + 1) unless present; returns 1 when newly inserted
+__device__ __forceinline__ uint32_t rep_insert(uint32_t* keys, uint32_t K, uint32_t key) {
+  volatile uint32_t* vk = keys;
+  uint32_t h = rep_hash(key, K);
+  for (;;) {
+    uint32_t k = vk[h];
+    if (k == key) return 0u;
+    if (k == 0u) {
+      k = atomicCAS(&keys[h], 0u, key);
+      if (k == 0u) return 1u;
+      if (k == key) return 0u;
+    }
+    h = (h + 1u == K) ? 0u : h + 1u;
+  }
+}
+
+__device__ __forceinline__ int rep_find(const uint32_t* keys, uint32_t K, uint32_t key) {
+  uint32_t h = rep_hash(key, K);
+  for (;;) {
+    const uint32_t k = keys[h];
+    if (k == key) return (int)h;
+    if (k == 0u) return -1;
+    h = (h + 1u == K) ? 0u : h + 1u;
+  }
+}
+
+// PASS 0: mark + collect repeats (returns via *s_ins / *s_ovf); PASS 1: exact count
+template <int T, int PASS>
+__device__ __forceinline__ void walk_cold(const Params& P, uint32_t* bm, uint32_t* keys, uint32_t* vals, uint32_t K,
+                                          const uint32_t* s_lo, const uint32_t* s_hi, const uint32_t* s_pfx, int nb,
+                                          uint32_t ngroups, uint32_t lo_rank, unsigned long long& tb,
+                                          unsigned long long& tu, uint32_t* s_ins) {
+  const uint4* adj4 = reinterpret_cast<const uint4*>(P.adj);
+  const uint32_t limit = K / 2u;
+  for (uint32_t g0 = threadIdx.x; g0 < ngroups; g0 += 2 * T) {
+    uint4 q[2];
+    uint32_t lo[2], hi[2], sg[2], p0[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint32_t g = g0 + (uint32_t)i * T;
+      lo[i] = 1u;
+      hi[i] = 0u;
+      sg[i] = 0u;
+      p0[i] = 0u;
+      q[i] = make_uint4(0u, 0u, 0u, 0u);
+      if (g < ngroups) {
+        const int k = find_record(s_pfx, nb, g);
+        const uint32_t lox = s_lo[k];
+        lo[i] = lox & 0x7fffffffu;
+        sg[i] = lox & 0x80000000u;
+        hi[i] = s_hi[k];
+        const uint32_t grp = (lo[i] >> 2) + (g - s_pfx[k]);
+        p0[i] = grp << 2;
+        q[i] = ld_stream(adj4 + grp);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint32_t wv[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t p = p0[i] + (uint32_t)j;
+        if (p >= lo[i] && p < hi[i]) {
+          const uint32_t rank = wv[j] & 0x7fffffffu;
+          if (PASS == 0) {
+            const uint32_t rel = rank - lo_rank;
+            const uint32_t bit = 1u << (rel & 31u);
+            const uint32_t old = atomicOr(&bm[rel >> 5], bit);
+            if ((old & bit) && *(volatile uint32_t*)s_ins < limit) {
+              if (rep_insert(keys, K, rank + 1u)) atomicAdd(s_ins, 1u);
+            }
+          } else {
+            const int slot = rep_find(keys, K, rank + 1u);
+            if (slot >= 0) {
+              const uint32_t sh = ((wv[j] ^ sg[i]) >> 31) << 4;
+              const uint32_t old = atomicAdd(&vals[slot], 1u << sh);
+              tb += (old >> sh) & 0xffffu;
+              tu += (old >> (sh ^ 16u)) & 0xffffu;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
 // Sparse band walk with at most two int4 groups per thread: both loads are issued before
 // either group is processed, and the touched counter words are kept in registers so the
 // zeroing pass needs neither the adjacency nor the record search again.
@@ -356,6 +457,7 @@ struct Smem {
   uint32_t* pfx;
   uint32_t* v;
   unsigned long long* w;
+  uint32_t* ins;  // repeat-set insertions of the current cold round
 };
 
 // General path: any degree (records in batches of T), table or binary search, layout W.
@@ -545,12 +647,63 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     if (ng) tile_round(0u, hstep, ng, bw);
   }
   if (P.phase == 1 || ncols <= hstep || (P.debug & 8)) return;
-  if (P.hslots != 0u) {
+  // cold range in seen-bitmap rounds of bm_cols columns (see walk_cold)
+  auto bitmap_rounds = [&]() {
+    uint32_t* bm = S.cnt;
+    uint32_t* keys = S.cnt + P.bm_words;
+    uint32_t* vals = keys + P.rep_slots;
+    const uint32_t K = P.rep_slots;
+    uint32_t hi = c1;
+    for (uint32_t c = hstep; c < ncols; c += P.bm_cols) {
+      const uint32_t cb = min(c + P.bm_cols, ncols);
+      const uint32_t lo = col(cb);
+      if (t0) *S.ins = 0u;  // published by setup's barriers
+      unsigned long long bw;
+      const uint32_t ng = setup(hi, lo, bw);
+      if (t0) work += bw;
+      hi = lo;
+      if (ng == 0u) continue;
+      const long long top = (long long)P.n - (long long)c * t16;
+      const long long bot = (long long)P.n - (long long)cb * t16;
+      const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
+      const uint32_t span_words = (uint32_t)((top - (long long)lo_rank + 31) / 32);
+      walk_cold<T, 0>(P, bm, keys, vals, K, S.lo, S.hi, S.pfx, nb, ng, lo_rank, tb, tu, S.ins);
+      __syncthreads();
+      const bool ovf = *S.ins >= K / 2u;
+      if (!ovf) walk_cold<T, 1>(P, bm, keys, vals, K, S.lo, S.hi, S.pfx, nb, ng, lo_rank, tb, tu, S.ins);
+      __syncthreads();
+      uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
+      for (uint32_t i = threadIdx.x; i < (span_words + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+      for (uint32_t i = threadIdx.x; i < (2u * K) / 4u; i += T) c4[P.bm_words / 4u + i] = make_uint4(0u, 0u, 0u, 0u);
+      __syncthreads();
+      if (ovf) {
+        // too many repeated end vertices for the set: counter tiles for these columns
+        uint32_t thi = col(c);
+        for (uint32_t cc = c; cc < cb; cc += step) {
+          const uint32_t tlo = col(min(cc + step, cb));
+          unsigned long long tbw;
+          const uint32_t tng = setup(thi, tlo, tbw);
+          if (tng) tile_round(cc, step, tng, tbw);
+          thi = tlo;
+        }
+      }
+    }
+  };
+
+  // cold range: one hash round if it fits; else seen-bitmap rounds when counter tiles
+  // would average fewer than 64 wedges per round (very wide, sparse end-vertex ranges,
+  // e.g. tens of millions of ranks); else counter tiles band by band
+  if (P.hslots != 0u || P.bm_cols != 0u) {
     unsigned long long wc;
     const uint32_t ng = setup(c1, cn, wc);
-    if (3ull * wc <= 2ull * P.hslots) {  // the whole cold range in one hash round (load <= 2/3)
+    if (P.hslots != 0u && 3ull * wc <= 2ull * P.hslots) {  // load <= 2/3
       if (t0) work += wc;
       if (ng) hash_round(ng, wc);
+      return;
+    }
+    const unsigned long long tile_rounds = (ncols - hstep + step - 1u) / step;
+    if (P.bm_cols != 0u && (wc < 64ull * tile_rounds || (P.debug & 512))) {  // 512: force (tests)
+      bitmap_rounds();
       return;
     }
   }
@@ -564,6 +717,7 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
   __shared__ uint32_t s_v[32];
   __shared__ unsigned long long s_w[33];
   __shared__ uint32_t s_task;
+  __shared__ uint32_t s_ins;
   Smem S;
   S.cnt = reinterpret_cast<uint32_t*>(smem4);
   S.lo = S.cnt + P.cap_words;
@@ -571,6 +725,7 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
   S.pfx = S.hi + T;
   S.v = s_v;
   S.w = s_w;
+  S.ins = &s_ins;
 
   for (uint32_t i = threadIdx.x; i < P.cap_words / 4; i += T) smem4[i] = make_uint4(0u, 0u, 0u, 0u);
 
@@ -776,6 +931,10 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     P.fast = (opts.flags & 1) ? 0 : 1;
     P.fast_max = two_phase ? (uint32_t)std::min(L.threads, Lc.threads) : (uint32_t)X.threads;
     P.hslots = (opts.flags & 2) ? 0u : (uint32_t)X.cap_words / 2u;
+    // cold seen-bitmap rounds (flags bit 7 disables): 1/8 of the tile for the repeat set
+    P.rep_slots = std::max(64u, ((uint32_t)X.cap_words / (P.debug & 256 ? 4u : 16u)) & ~3u);
+    P.bm_words = ((uint32_t)X.cap_words - 2u * P.rep_slots) & ~3u;
+    P.bm_cols = (opts.flags & 128) ? 0u : (32u * P.bm_words) / std::max(1u, g.t16);
     P.debug = opts.flags;
     P.dynamic = opts.algo == BBC_ALGO_GBBCPP;
     P.acc = g.acc;
