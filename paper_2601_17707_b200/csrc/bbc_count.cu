@@ -551,15 +551,25 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   const uint32_t ncols = min(P.nbands, (P.n - 1u - r) / t16 + 1u);  // columns holding ranks > r
   const int nb = (int)(re - rb);
   const bool mine = (int)threadIdx.x < nb;
-  uint32_t recx = 0u;
+  uint32_t recx = 0u, lend = 0u;
   const uint32_t* row = P.bnd;
   if (mine) {
     const uint2 rr = P.rec[rb + threadIdx.x];
     recx = rr.x;
-    row = P.bnd + (size_t)rr.y * P.nbands;
+    if (P.bnd)
+      row = P.bnd + (size_t)rr.y * P.nbands;
+    else
+      lend = __ldg(P.coff + rr.y + 1);
   }
-  // table column j of this thread's record (0 past the last column: start of the list)
-  auto col = [&](uint32_t j) -> uint32_t { return (mine && j < P.nbands) ? __ldg(row + j) : 0u; };
+  // column j of this thread's record: first position of its list with rank >= n - j * t16
+  // (0 past the last column: start of the list), from the band table or, without one
+  // (end-vertex ranges too wide for a table), by binary search within the admitted suffix
+  auto col = [&](uint32_t j) -> uint32_t {
+    if (!mine || j >= P.nbands) return 0u;
+    if (P.bnd) return __ldg(row + j);
+    if (j == 0u) return lend;
+    return lower_bound_rank(P.adj, recx & 0x7fffffffu, lend, (long long)P.n - (long long)j * t16);
+  };
   // columns needed up front are loaded together (one latency)
   const uint32_t c0 = P.phase == 2 ? 0u : col(0u), c1 = col(hstep);
   const uint32_t c2 = P.phase == 1 ? 0u : col(min(hstep + step, ncols));
@@ -752,7 +762,7 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
     unsigned long long tb = 0, tu = 0;
     // fast path: every record held by one thread; the bound is the same for all launches of
     // a count so that phases agree on which anchors they split
-    const bool fast = P.fast && P.bnd != nullptr && deg <= min((uint32_t)T, P.fast_max);
+    const bool fast = P.fast && deg <= min((uint32_t)T, P.fast_max);
     if (!fast && P.phase == 2) {  // general-path anchors are done entirely in phase 1
       __syncthreads();
       continue;
@@ -874,7 +884,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
   Launch L, Lc;
   int rc = configure(g, L);
   if (rc) return rc;
-  bool use_table = g.bnd != nullptr;
+  bool use_table = g.bnd != nullptr && !(opts.flags & 1024);  // 1024: binary search (tests)
   const bool tile_override = opts.tile_span > 0 && (uint32_t)opts.tile_span < 2u * ((uint32_t)L.cap_words - 8u);
   if (tile_override) use_table = false;
   // flags bit 6 (experimental, measured slower on config 2): hub band and cold range in
@@ -928,7 +938,8 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     P.span16 = span16;
     P.span32 = span32;
     P.cap_words = (uint32_t)X.cap_words;
-    P.fast = (opts.flags & 1) ? 0 : 1;
+    // the fast path needs the fixed column grid: not with TileConfig.tile_size spans
+    P.fast = ((opts.flags & 1) || tile_override || g.t16 == 0) ? 0 : 1;
     P.fast_max = two_phase ? (uint32_t)std::min(L.threads, Lc.threads) : (uint32_t)X.threads;
     P.hslots = (opts.flags & 2) ? 0u : (uint32_t)X.cap_words / 2u;
     // cold seen-bitmap rounds (flags bit 7 disables): 1/8 of the tile for the repeat set

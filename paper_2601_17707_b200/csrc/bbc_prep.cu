@@ -408,7 +408,9 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     const size_t need = (size_t)nc * g.nbands * 4;
-    if (nc > 0 && n > 0 && need <= std::min<size_t>((size_t)8 << 30, free_b / 4)) {
+    size_t budget = (size_t)2048 << 20;  // env BBC_TABLE_MB; beyond it the kernel searches
+    if (const char* e = std::getenv("BBC_TABLE_MB")) budget = (size_t)std::atoll(e) << 20;
+    if (nc > 0 && n > 0 && need <= std::min<size_t>(budget, free_b / 4)) {
       BBC_ALLOC(g.bnd, need);
       k_band_table<<<grid_for(nc * (int64_t)g.nbands, sms), kThreads, 0, st>>>(g.adj, g.coff, nc, g.nbands, g.t16,
                                                                                  (uint32_t)n, g.bnd);

@@ -73,7 +73,8 @@ def test_synthetic_configs_vs_reference(gpu, golden, key):
             g = DeviceGraph.from_host(cfg.n_u, cfg.n_v, u, v, s, 0, side)
             # every cold-range strategy: default, general banded path, no hash, forced
             # seen-bitmap rounds (small / large repeat set), tiles only, two launches
-            for flags in (0, _lib.FLAG_BANDED_ONLY, 2, 2 | 512, 2 | 512 | 256, 2 | 128, 64):
+            # (1024: band boundaries by binary search instead of the table)
+            for flags in (0, _lib.FLAG_BANDED_ONLY, 2, 2 | 512, 2 | 512 | 256, 2 | 128, 64, 1024, 1024 | 2 | 512):
                 r = g.count(algo, flags=flags)
                 assert (r.balanced, r.unbalanced) == (rec["balanced"], rec["unbalanced"]), (key, side, algo, flags)
                 assert r.wedges == r.wedges_total == (rec["w_u"] if g.anchor_side == 0 else rec["w_v"])
