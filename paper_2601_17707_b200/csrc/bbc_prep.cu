@@ -185,10 +185,16 @@ __global__ void k_anchor_work(const uint2* __restrict__ rec, const uint32_t* __r
   }
 }
 
+// All device memory of a handle is stream-ordered (cudaMallocAsync on the handle's
+// stream) from the device's default pool, which keeps freed blocks cached: the
+// preprocessing temporaries of repeated graph builds (bench e2e) then cost no
+// cudaMalloc / cudaFree round trips.
+thread_local cudaStream_t t_alloc_stream = nullptr;
+
 struct DevBuf {
   void* p = nullptr;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, t_alloc_stream);
   }
   template <typename T>
   T* as() {
@@ -197,7 +203,7 @@ struct DevBuf {
 };
 
 int alloc(void** p, size_t bytes) {
-  cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+  cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, t_alloc_stream);
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error(std::string("device allocation of ") + std::to_string(bytes) + " bytes failed: " +
@@ -214,17 +220,11 @@ int alloc(void** p, size_t bytes) {
   } while (0)
 
 void free_graph_arrays(Graph& g) {
-  cudaFree(g.adj);
-  cudaFree(g.coff);
-  cudaFree(g.rec);
-  cudaFree(g.aoff);
-  cudaFree(g.awork);
-  cudaFree(g.order);
-  cudaFree(g.rank_to_id);
-  cudaFree(g.acc);
-  cudaFree(g.queue);
-  cudaFree(g.block_work);
-  cudaFree(g.bnd);
+  void* ptrs[] = {g.adj, g.coff, g.rec, g.aoff, g.awork, g.order, g.rank_to_id, g.acc, g.queue, g.bnd};
+  for (void* p : ptrs)
+    if (p) cudaFreeAsync(p, g.stream);
+  cudaFree(g.block_work);  // (re)allocated with cudaMalloc by the count
+  cudaStreamSynchronize(g.stream);
   g.bnd = nullptr;
   g.adj = g.coff = g.aoff = g.order = g.rank_to_id = nullptr;
   g.rec = nullptr;
@@ -453,6 +453,14 @@ int init_handle(Graph& g, int device, int64_t n_u, int64_t n_v, int64_t m) {
     if (t == 128 || t == 256 || t == 512 || t == 1024) g.threads = t;
   }
   BBC_CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;  // keep freed blocks for the next build
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   BBC_CK(cudaEventCreate(&g.ev0));
   BBC_CK(cudaEventCreate(&g.ev1));
   return BBC_OK;
@@ -480,13 +488,15 @@ int create_common(int device, int64_t n_u, int64_t n_v, int64_t m, const int32_t
     delete h;
     return rc;
   }
+  t_alloc_stream = g.stream;
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  {  // upload buffers are released (stream-ordered) before any error teardown
   DevBuf du, dv, ds;
   const int32_t* pu = u;
   const int32_t* pv = v;
   const int8_t* ps = s;
-  cudaEvent_t t0, t1;
-  cudaEventCreate(&t0);
-  cudaEventCreate(&t1);
   if (host && m > 0) {
     rc = alloc(&du.p, (size_t)m * 4);
     if (!rc) rc = alloc(&dv.p, (size_t)m * 4);
@@ -507,6 +517,7 @@ int create_common(int device, int64_t n_u, int64_t n_v, int64_t m, const int32_t
     cudaEventRecord(t1, g.stream);
     cudaEventSynchronize(t1);
     cudaEventElapsedTime(&g.preprocess_ms, t0, t1);
+  }
   }
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);
