@@ -194,7 +194,9 @@ def main():
     g = _lib.DeviceGraph.from_device_ptrs(cfg.n_u, cfg.n_v, m, du.data_ptr(), dv.data_ptr(), ds.data_ptr(), local)
     algo = _lib.ALGO_GBBCPP if args.algo == "gbbc++" else _lib.ALGO_GBBC
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
-    red = torch.zeros(6, dtype=torch.int64, device="cuda")
+    from paper_2601_17707_b200.distributed import from_limbs, to_limbs
+
+    red = torch.zeros(8, dtype=torch.int64, device="cuda")
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def step():
@@ -203,17 +205,14 @@ def main():
         r = g.count(algo, part_index=rank, part_count=world)
         ms = r.count_ms
         if world > 1:
-            vals = [r.balanced & 0xFFFFFFFF, (r.balanced >> 32) & 0xFFFFFFFF, r.balanced >> 64,
-                    r.unbalanced & 0xFFFFFFFF, (r.unbalanced >> 32) & 0xFFFFFFFF, r.unbalanced >> 64]
-            red.copy_(torch.tensor(vals, dtype=torch.int64))
+            # one NCCL all-reduce of the two 128-bit counts as 32-bit limbs (exact)
+            red.copy_(torch.tensor(to_limbs([r.balanced, r.unbalanced]), dtype=torch.int64))
             ev0.record()
             dist.all_reduce(red)
             ev1.record()
             ev1.synchronize()
             ms += ev0.elapsed_time(ev1)
-            t = red.tolist()
-            bal = t[0] + (t[1] << 32) + (t[2] << 64)
-            unb = t[3] + (t[4] << 32) + (t[5] << 64)
+            bal, unb = from_limbs(red.tolist())
         else:
             bal, unb = r.balanced, r.unbalanced
         return ms, bal, unb, r
@@ -260,9 +259,9 @@ def main():
         h = ctypes_create(pu, pv, ps, cfg, local)
         r2 = h.count(algo, part_index=rank, part_count=world)
         if world > 1:
-            red.copy_(torch.tensor([r2.balanced & 0xFFFFFFFF, r2.balanced >> 32, 0, 0, 0, 0], dtype=torch.int64))
+            red.copy_(torch.tensor(to_limbs([r2.balanced, r2.unbalanced]), dtype=torch.int64))
             dist.all_reduce(red)
-            red.tolist()
+            from_limbs(red.tolist())
         dt = time.perf_counter() - t0
         h.close()
         if i >= args.warmup:
