@@ -306,7 +306,7 @@ __device__ __forceinline__ int rep_find(const uint32_t* keys, uint32_t K, uint32
   }
 }
 
-// PASS 0: mark + collect repeats (returns via *s_ins / *s_ovf); PASS 1: exact count
+// PASS 0: mark + collect repeats (insertions counted in *s_ins); PASS 1: exact count.
 template <int T, int PASS>
 __device__ __forceinline__ void walk_cold(const Params& P, uint32_t* bm, uint32_t* keys, uint32_t* vals, uint32_t K,
                                           const uint32_t* s_lo, const uint32_t* s_hi, const uint32_t* s_pfx, int nb,
@@ -702,7 +702,9 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
 
   // cold range: one hash round if it fits; else seen-bitmap rounds when counter tiles
   // would average fewer than 64 wedges per round (very wide, sparse end-vertex ranges,
-  // e.g. tens of millions of ranks); else counter tiles band by band
+  // e.g. tens of millions of ranks); else counter tiles band by band.  (A single
+  // hashed-filter round for medium anchors was measured slower than tiles: probe
+  // divergence and two passes.)
   if (P.hslots != 0u || P.bm_cols != 0u) {
     unsigned long long wc;
     const uint32_t ng = setup(c1, cn, wc);
