@@ -46,7 +46,8 @@ struct Params {
   const uint32_t* __restrict__ aoff;
   const unsigned long long* __restrict__ awork;
   const uint32_t* __restrict__ order;
-  const uint32_t* __restrict__ bnd;  // nullptr: binary search
+  const uint32_t* __restrict__ bnd;   // nullptr: binary search
+  const uint32_t* __restrict__ brow;  // row of each centre in bnd (~0: binary search)
   uint32_t nbands;
   uint32_t n;
   uint32_t ntasks;
@@ -485,8 +486,9 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
         const uint2 rr = P.rec[b0 + threadIdx.x];
         const uint32_t begin = rr.x & 0x7fffffffu, c = rr.y;
         uint32_t lo, hi;
-        if (table) {
-          const uint32_t* row = P.bnd + (size_t)c * P.nbands;
+        const uint32_t bi = table ? __ldg(P.brow + c) : 0xffffffffu;
+        if (bi != 0xffffffffu) {
+          const uint32_t* row = P.bnd + (size_t)bi * P.nbands;
           const uint32_t j0 = b * step, j1 = (b + 1u) * step;
           hi = __ldg(row + j0);
           lo = j1 < P.nbands ? __ldg(row + j1) : 0u;
@@ -552,12 +554,13 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   const int nb = (int)(re - rb);
   const bool mine = (int)threadIdx.x < nb;
   uint32_t recx = 0u, lend = 0u;
-  const uint32_t* row = P.bnd;
+  const uint32_t* row = nullptr;
   if (mine) {
     const uint2 rr = P.rec[rb + threadIdx.x];
     recx = rr.x;
-    if (P.bnd)
-      row = P.bnd + (size_t)rr.y * P.nbands;
+    const uint32_t bi = P.bnd ? __ldg(P.brow + rr.y) : 0xffffffffu;
+    if (bi != 0xffffffffu)
+      row = P.bnd + (size_t)bi * P.nbands;
     else
       lend = __ldg(P.coff + rr.y + 1);
   }
@@ -566,7 +569,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   // (end-vertex ranges too wide for a table), by binary search within the admitted suffix
   auto col = [&](uint32_t j) -> uint32_t {
     if (!mine || j >= P.nbands) return 0u;
-    if (P.bnd) return __ldg(row + j);
+    if (row) return __ldg(row + j);
     if (j == 0u) return lend;
     return lower_bound_rank(P.adj, recx & 0x7fffffffu, lend, (long long)P.n - (long long)j * t16);
   };
@@ -927,6 +930,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     P.awork = g.awork;
     P.order = g.order;
     P.bnd = use_table ? g.bnd : nullptr;
+    P.brow = g.brow;
     P.nbands = g.nbands;
     P.t16 = g.t16;
     P.bcols16 = std::max(1u, span16 / std::max(1u, g.t16));

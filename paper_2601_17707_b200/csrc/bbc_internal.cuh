@@ -40,7 +40,8 @@ struct Graph {
   unsigned long long* awork = nullptr;
   uint32_t* order = nullptr;
   uint32_t* rank_to_id = nullptr;
-  uint32_t* bnd = nullptr;
+  uint32_t* bnd = nullptr;   // band-table rows (long centre lists only)
+  uint32_t* brow = nullptr;  // brow[c]: row of centre c in bnd, or ~0 (binary search)
   uint32_t nbands = 0;
   uint32_t t16 = 0;
   // count scratch

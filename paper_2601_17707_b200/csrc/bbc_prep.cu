@@ -141,13 +141,45 @@ __global__ void k_records(const uint32_t* __restrict__ pos_sorted, const unsigne
   }
 }
 
-// band table: row c holds, for j in [0, nbands), the first position of c's list whose
-// rank is >= n - j * t (j = 0: the list end).  Lists are rank-sorted.
-__global__ void k_band_table(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ coff, int64_t nc,
-                             uint32_t nbands, uint32_t t, uint32_t n, uint32_t* __restrict__ bnd) {
+// centres with list length > {0, 4, 16, 64, 256, 1024, 4096, 16384}
+__global__ void k_count_rows(const uint32_t* __restrict__ coff, int64_t nc, unsigned int* __restrict__ cnt) {
+  unsigned int c8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t d = coff[c + 1] - coff[c];
+    c8[0] += d > 0u;
+    c8[1] += d > 4u;
+    c8[2] += d > 16u;
+    c8[3] += d > 64u;
+    c8[4] += d > 256u;
+    c8[5] += d > 1024u;
+    c8[6] += d > 4096u;
+    c8[7] += d > 16384u;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    unsigned int v = c8[i];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&cnt[i], v);
+  }
+}
+
+// table rows for centres with lists longer than min_deg (row order is arbitrary)
+__global__ void k_table_rows(const uint32_t* __restrict__ coff, int64_t nc, uint32_t min_deg,
+                             uint32_t* __restrict__ brow, unsigned int* __restrict__ rows) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x)
+    brow[c] = (coff[c + 1] - coff[c] > min_deg) ? atomicAdd(rows, 1u) : 0xffffffffu;
+}
+
+// band table: row brow[c] holds, for j in [0, nbands), the first position of c's list
+// whose rank is >= n - j * t (j = 0: the list end).  Lists are rank-sorted.
+__global__ void k_band_table(const uint32_t* __restrict__ adj, const uint32_t* __restrict__ coff,
+                             const uint32_t* __restrict__ brow, int64_t nc, uint32_t nbands, uint32_t t, uint32_t n,
+                             uint32_t* __restrict__ bnd) {
   const int64_t total = nc * (int64_t)nbands;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / nbands;
+    const uint32_t row = brow[c];
+    if (row == 0xffffffffu) continue;
     const uint32_t j = (uint32_t)(e - c * nbands);
     uint32_t lo = coff[c], hi = coff[c + 1];
     if (j > 0) {
@@ -164,7 +196,7 @@ __global__ void k_band_table(const uint32_t* __restrict__ adj, const uint32_t* _
         }
       }
     }
-    bnd[e] = hi;
+    bnd[(size_t)row * nbands + j] = hi;
   }
 }
 
@@ -220,12 +252,13 @@ int alloc(void** p, size_t bytes) {
   } while (0)
 
 void free_graph_arrays(Graph& g) {
-  void* ptrs[] = {g.adj, g.coff, g.rec, g.aoff, g.awork, g.order, g.rank_to_id, g.acc, g.queue, g.bnd};
+  void* ptrs[] = {g.adj, g.coff, g.rec, g.aoff, g.awork, g.order, g.rank_to_id, g.acc, g.queue, g.bnd, g.brow};
   for (void* p : ptrs)
     if (p) cudaFreeAsync(p, g.stream);
   cudaFree(g.block_work);  // (re)allocated with cudaMalloc by the count
   cudaStreamSynchronize(g.stream);
   g.bnd = nullptr;
+  g.brow = nullptr;
   g.adj = g.coff = g.aoff = g.order = g.rank_to_id = nullptr;
   g.rec = nullptr;
   g.awork = g.acc = g.block_work = nullptr;
@@ -398,23 +431,49 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
   }
   BBC_CK(cudaGetLastError());
 
-  // band table: only when it fits a modest memory budget
+  // band table: rows only for centres whose list is longer than
+  // kTableMinDeg (short lists are binary-searched within one or two cache lines), and
+  // only when the rows fit a memory budget; brow[c] = row of c or ~0.
   {
     int span16 = count_span16(g);
     if (span16 <= 0) return BBC_ERR_CUDA;
     g.t16 = (uint32_t)span16;
     g.nbands = (uint32_t)((n + span16 - 1) / span16);
     if (g.nbands == 0) g.nbands = 1;
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const size_t need = (size_t)nc * g.nbands * 4;
-    size_t budget = (size_t)2048 << 20;  // env BBC_TABLE_MB; beyond it the kernel searches
-    if (const char* e = std::getenv("BBC_TABLE_MB")) budget = (size_t)std::atoll(e) << 20;
-    if (nc > 0 && n > 0 && need <= std::min<size_t>(budget, free_b / 4)) {
-      BBC_ALLOC(g.bnd, need);
-      k_band_table<<<grid_for(nc * (int64_t)g.nbands, sms), kThreads, 0, st>>>(g.adj, g.coff, nc, g.nbands, g.t16,
-                                                                                 (uint32_t)n, g.bnd);
-      BBC_CK(cudaGetLastError());
+    if (nc > 0 && n > 0) {
+      size_t free_b = 0, total_b = 0;
+      cudaMemGetInfo(&free_b, &total_b);
+      size_t budget = (size_t)8192 << 20;  // env BBC_TABLE_MB; beyond it the kernel searches
+      if (const char* e = std::getenv("BBC_TABLE_MB")) budget = (size_t)std::atoll(e) << 20;
+      budget = std::min<size_t>(budget, free_b / 4);
+      // smallest list-length threshold whose rows fit the budget (0: every centre)
+      DevBuf rowcnt;
+      BBC_ALLOC(rowcnt.p, 64);
+      const uint32_t thresholds[8] = {0u, 4u, 16u, 64u, 256u, 1024u, 4096u, 16384u};
+      BBC_CK(cudaMemsetAsync(rowcnt.p, 0, 64, st));
+      k_count_rows<<<grid_for(nc, sms), kThreads, 0, st>>>(g.coff, nc, rowcnt.as<unsigned int>());
+      unsigned int cnt[8];
+      BBC_CK(cudaMemcpyAsync(cnt, rowcnt.p, 32, cudaMemcpyDeviceToHost, st));
+      BBC_CK(cudaStreamSynchronize(st));
+      int pick = -1;
+      for (int i = 0; i < 8 && pick < 0; ++i)
+        if ((size_t)cnt[i] * g.nbands * 4 <= budget) pick = i;
+      unsigned int rows = 0;
+      if (pick >= 0 && cnt[pick] > 0) {
+        BBC_ALLOC(g.brow, (size_t)(nc + 1) * 4);
+        BBC_CK(cudaMemsetAsync(rowcnt.p, 0, 16, st));
+        k_table_rows<<<grid_for(nc, sms), kThreads, 0, st>>>(g.coff, nc, thresholds[pick], g.brow,
+                                                             rowcnt.as<unsigned int>());
+        BBC_CK(cudaMemcpyAsync(&rows, rowcnt.p, 4, cudaMemcpyDeviceToHost, st));
+        BBC_CK(cudaStreamSynchronize(st));
+      }
+      const size_t need = (size_t)rows * g.nbands * 4;
+      if (rows > 0 && need <= budget) {
+        BBC_ALLOC(g.bnd, need);
+        k_band_table<<<grid_for(nc * (int64_t)g.nbands, sms), kThreads, 0, st>>>(
+            g.adj, g.coff, g.brow, nc, g.nbands, g.t16, (uint32_t)n, g.bnd);
+        BBC_CK(cudaGetLastError());
+      }
     }
   }
 
