@@ -111,6 +111,12 @@ int bbc_count(bbc_graph* g, const bbc_opts* opts, uint64_t out[2], bbc_stats* st
 /* Per-CTA admitted wedges of the last bbc_count (ScheduleReport.per_block_work). */
 int bbc_block_work(bbc_graph* g, uint64_t* out, int32_t n);
 
+/* Diagnostics: rounds of the last bbc_count run with opts.flags bit 12 (BBC_FLAG_ROUNDS):
+ * out[0] bitmap rounds, out[1] of them overflowed and redone, out[2] counter-tile rounds,
+ * out[3] hash rounds (the per-anchor round kinds of DESIGN.md section 4), out[4] int4
+ * groups walked, out[5] wedges walked, out[6] round set-ups (block scans), out[7] 0. */
+int bbc_round_counters(bbc_graph* g, uint64_t out[8]);
+
 /* Anchor dispatch order of `algo` as anchor-side vertex ids (ScheduleReport.task_order);
  * `work` (nullable) receives each task's admitted wedges in the same order. */
 int bbc_task_order(bbc_graph* g, int32_t algo, int32_t* ids, uint64_t* work, int64_t n);

@@ -27,10 +27,11 @@ SIDE_U = 0
 SIDE_V = 1
 SIDE_MIN = 2
 FLAG_BANDED_ONLY = 1
+FLAG_ROUNDS = 4096  # record per-kind round counters (round_counters())
 
 EXPORTED_SYMBOLS = (
     "bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work", "bbc_task_order",
-    "bbc_graph_info", "bbc_graph_stream", "bbc_graph_destroy", "bbc_device_count", "bbc_last_error",
+    "bbc_round_counters", "bbc_graph_info", "bbc_graph_stream", "bbc_graph_destroy", "bbc_device_count", "bbc_last_error",
     "bbc_last_error_info",
 )
 
@@ -68,6 +69,7 @@ def load() -> ctypes.CDLL:
         L.bbc_count.argtypes = [P, ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
         L.bbc_block_work.argtypes = [P, U64P, I32]
         L.bbc_task_order.argtypes = [P, I32, ctypes.POINTER(ctypes.c_int32), P, I64]
+        L.bbc_round_counters.argtypes = [P, U64P]
         L.bbc_graph_info.argtypes = [P, ctypes.POINTER(ctypes.c_int64), I32]
         L.bbc_graph_stream.argtypes = [P]
         L.bbc_graph_stream.restype = P
@@ -77,7 +79,7 @@ def load() -> ctypes.CDLL:
         L.bbc_last_error.restype = ctypes.c_char_p
         L.bbc_last_error_info.restype = ctypes.c_int64
         for name in ("bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work",
-                     "bbc_task_order", "bbc_graph_info", "bbc_device_count"):
+                     "bbc_task_order", "bbc_round_counters", "bbc_graph_info", "bbc_device_count"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
         return L
@@ -179,6 +181,15 @@ class DeviceGraph:
         if rc:
             _raise(rc)
         return [int(buf[i]) for i in range(n)]
+
+    def round_counters(self) -> dict[str, int]:
+        """Rounds of the last count run with FLAG_ROUNDS, by kind."""
+        buf = (ctypes.c_uint64 * 8)()
+        rc = load().bbc_round_counters(self._h, buf)
+        if rc:
+            _raise(rc)
+        return dict(zip(("bitmap", "bitmap_redone", "tile", "hash", "groups", "wedges", "setups"),
+                        (int(x) for x in buf)))
 
     def task_order(self, algo: int) -> tuple[np.ndarray, np.ndarray]:
         """(anchor ids, admitted wedges) in the dispatch order of ``algo``."""

@@ -53,6 +53,15 @@ int bbc_block_work(bbc_graph* h, uint64_t* out, int32_t n) {
   return BBC_OK;
 }
 
+int bbc_round_counters(bbc_graph* h, uint64_t out[8]) {
+  if (!h || !out) {
+    bbc::set_error("bad arguments to bbc_round_counters");
+    return BBC_ERR_ARG;
+  }
+  for (int i = 0; i < 8; ++i) out[i] = h->g.rounds[i];
+  return BBC_OK;
+}
+
 int bbc_task_order(bbc_graph* h, int32_t algo, int32_t* out, uint64_t* work, int64_t n) {
   if (!h || !out || n < 0) {
     bbc::set_error("bad arguments to bbc_task_order");

@@ -27,6 +27,7 @@
 // Sub-slices of each record within a band come from the band table (one load per edge
 // of the band) or, without a table, from a binary search.
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "bbc_internal.cuh"
@@ -64,8 +65,11 @@ struct Params {
   uint32_t bcols16;
   int phase;        // 0: every band; 1: hub band only; 2: cold range only
   uint32_t bm_cols;    // cold seen-bitmap round width in table columns (0: off)
-  uint32_t bm_words;   // bitmap words (start of the repeat set)
-  uint32_t rep_slots;  // repeat-set slots (keys, then packed counts)
+  uint32_t bm_words;   // bitmap words of the widest round
+  uint32_t bm_cols0;   // first bitmap round width in table columns
+  uint32_t rep_slots;  // repeat-queue entries left by the widest bitmap round
+  uint32_t bits_thr;   // cold range in bitmap rounds when tile rounds would average fewer wedges
+  uint32_t sweep_min;  // tile rounds with >= sweep_min wedges per counter word close by sweep
   uint32_t fast_max;  // largest degree on the fast path (same for every launch of a count)
   int debug;        // flags bits 2 / 3: skip band 0 / skip the cold range (timing only)
   int dynamic;
@@ -248,168 +252,173 @@ __device__ __forceinline__ void hash_bump_close(uint32_t* tab, uint32_t K, uint3
   tu += (old >> (sh ^ 16u)) & 0xffffu;
 }
 
-template <int T>
-__device__ __forceinline__ void walk_hash(const Params& P, uint32_t* tab, uint32_t K, const uint32_t* s_lo,
-                                          const uint32_t* s_hi, const uint32_t* s_pfx, int nb, uint32_t ngroups,
-                                          unsigned long long& tb, unsigned long long& tu) {
+// ---- shared-memory primitives on 32-bit shared addresses ------------------------------
+// (generic pointers make the compiler re-derive the shared window base per access)
+__device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t s_atom_add(uint32_t a, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ uint32_t s_atom_or(uint32_t a, uint32_t v) {
+  uint32_t r;
+  asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
+  return r;
+}
+__device__ __forceinline__ void s_red_add(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void s_st(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// valid slots (bits 0..3) of the int4 group starting at word position p0 for [lo, hi)
+__device__ __forceinline__ uint32_t slot_mask(uint32_t p0, uint32_t lo, uint32_t hi) {
+  const int a = max((int)(lo - p0), 0);
+  const int b = min((int)(hi - p0), 4);
+  return b <= a ? 0u : (((1u << b) - 1u) & (0xfu << a));
+}
+
+// Walk the int4 groups of the round's sub-slices, a PAIR of consecutive groups per thread
+// per iteration (one record search per pair; the second group usually lies in the same
+// record).  Both loads are issued before either group is processed.  op.wedge(word,
+// sign, slot) runs for every valid wedge; op.flush() after each pair.
+template <int T, class Op>
+__device__ __forceinline__ void walk_pairs(const Params& P, const uint32_t* s_lo, const uint32_t* s_hi,
+                                           const uint32_t* s_pfx, int nb, uint32_t ngroups, Op& op) {
   const uint4* adj4 = reinterpret_cast<const uint4*>(P.adj);
-  for (uint32_t g = threadIdx.x; g < ngroups; g += T) {
+  const uint32_t npairs = (ngroups + 1u) >> 1;
+  for (uint32_t gp = threadIdx.x; gp < npairs; gp += T) {
+    const uint32_t g = gp << 1;
     const int k = find_record(s_pfx, nb, g);
-    const uint32_t lox = s_lo[k];
-    const uint32_t lo = lox & 0x7fffffffu, sgn = lox & 0x80000000u, hi = s_hi[k];
-    const uint32_t grp = (lo >> 2) + (g - s_pfx[k]);
-    const uint4 q = ld_stream(adj4 + grp);
-    const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
-    const uint32_t p0 = grp << 2;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t p = p0 + (uint32_t)j;
-      if (p >= lo && p < hi) hash_bump_close(tab, K, wv[j] & 0x7fffffffu, (wv[j] ^ sgn) >> 31, tb, tu);
+    const uint32_t lx0 = s_lo[k], hi0 = s_hi[k];
+    const uint32_t lo0 = lx0 & 0x7fffffffu, sg0 = lx0 & 0x80000000u;
+    const uint32_t grp0 = (lo0 >> 2) + (g - s_pfx[k]);
+    const bool has1 = g + 1u < ngroups;
+    uint32_t lo1 = lo0, hi1 = hi0, sg1 = sg0, grp1 = grp0 + 1u;
+    if (has1 && k + 1 < nb && s_pfx[k + 1] <= g + 1u) {
+      int k1 = k + 1;
+      while (k1 + 1 < nb && s_pfx[k1 + 1] <= g + 1u) ++k1;
+      const uint32_t lx1 = s_lo[k1];
+      lo1 = lx1 & 0x7fffffffu;
+      sg1 = lx1 & 0x80000000u;
+      hi1 = s_hi[k1];
+      grp1 = (lo1 >> 2) + (g + 1u - s_pfx[k1]);
     }
+    const uint4 q0 = ld_stream(adj4 + grp0);
+    const uint4 q1 = has1 ? ld_stream(adj4 + grp1) : make_uint4(0u, 0u, 0u, 0u);
+    const uint32_t m = slot_mask(grp0 << 2, lo0, hi0) | (has1 ? slot_mask(grp1 << 2, lo1, hi1) << 4 : 0u);
+    const uint32_t wv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (m & (1u << j)) op.wedge(wv[j], j < 4 ? sg0 : sg1, j);
+    op.flush();
   }
 }
 
-// ---- cold bands: seen-bitmap + repeat set ---------------------------------------------
-// In the cold end-vertex range almost every (anchor, end vertex) pair has one common
-// centre, and a pair with one wedge contributes nothing.  A cold round therefore walks
-// its wedges twice: pass A sets one bit per end vertex (16x denser than a u8x2 counter,
-// so one round spans 16x more ranks) and inserts an end vertex into a small hash set
-// when its bit was already set; pass B counts exactly, in that set, every wedge whose end
-// vertex repeats, closing inline from the add's return value.  If the set would exceed
-// half its slots the round falls back to counter tiles.
-__device__ __forceinline__ uint32_t rep_hash(uint32_t key, uint32_t K) {
-  return (uint32_t)(((unsigned long long)(key * 0x9E3779B1u) * K) >> 32);
-}
+// counter-tile increments without return (closed later by the sweep)
+template <int W>
+struct OpTileDense {
+  uint32_t base, lo_rank;
+  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
+    const uint32_t rel = (w & 0x7fffffffu) - lo_rank, par = (w ^ sg) >> 31;
+    if (W == 8)
+      s_red_add(base + ((rel >> 1) << 2), 1u << (((rel & 1u) << 4) | (par << 3)));
+    else
+      s_red_add(base + (rel << 2), 1u << (par << 4));
+  }
+  __device__ __forceinline__ void flush() {}
+};
 
-// insert key (rank + 1) unless present; returns 1 when newly inserted
+// counter-tile increments closed inline from the return value (a + wedge adds the old
+// positive count to balanced and the old negative count to unbalanced, a - wedge the
+// reverse); 32-bit partial sums per pair (8 x 65535 < 2^32), flushed to 64 bits.  With
+// KEEP the touched word of each slot is kept (single-iteration rounds zero from it).
+template <int W, bool KEEP>
+struct OpTileClose {
+  uint32_t base, lo_rank;
+  unsigned long long *tb, *tu;
+  uint32_t b32 = 0, u32 = 0;
+  uint32_t touched[8];
+  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int j) {
+    const uint32_t rel = (w & 0x7fffffffu) - lo_rank, par = (w ^ sg) >> 31;
+    if (W == 8) {
+      const uint32_t sh = ((rel & 1u) << 4) | (par << 3);
+      const uint32_t a = base + ((rel >> 1) << 2);
+      const uint32_t old = s_atom_add(a, 1u << sh);
+      b32 += (old >> sh) & 0xffu;
+      u32 += (old >> (sh ^ 8u)) & 0xffu;
+      if (KEEP) touched[j] = a;
+    } else {
+      const uint32_t sh = par << 4;
+      const uint32_t a = base + (rel << 2);
+      const uint32_t old = s_atom_add(a, 1u << sh);
+      b32 += (old >> sh) & 0xffffu;
+      u32 += (old >> (sh ^ 16u)) & 0xffffu;
+      if (KEEP) touched[j] = a;
+    }
+  }
+  __device__ __forceinline__ void flush() {
+    *tb += b32;
+    *tu += u32;
+    b32 = u32 = 0u;
+  }
+};
+
+// cold-range hash round: key = rank + 1 in word 2i, packed u16 counts in word 2i + 1
+struct OpHash {
+  uint32_t* tab;
+  uint32_t K;
+  unsigned long long *tb, *tu;
+  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
+    hash_bump_close(tab, K, w & 0x7fffffffu, (w ^ sg) >> 31, *tb, *tu);
+  }
+  __device__ __forceinline__ void flush() {}
+};
+
+// ---- cold bands: two-bit seen/parity bitmap + repeat queue -----------------------------
+// In the cold end-vertex range almost every (anchor, end vertex) pair has one common
+// centre (config 2: 2.7 % of the cold wedges land on a repeated end vertex), and a pair
+// with one wedge contributes nothing.  A cold round therefore keeps two bits per end
+// vertex (8x denser than a u8x2 counter tile, so one round spans 8x more ranks):
+//   bit 0: seen;  bit 1: parity (1 = negative) of the FIRST wedge.
+// Every wedge ORs in its seen bit and, when negative, the parity bit, in ONE atomic.  A
+// wedge that finds the seen bit already set is a repeat and is appended to a queue as
+// (rank, counted parity): a negative repeat that turned the parity bit from 0 to 1 is
+// queued as POSITIVE -- it stands for the positive first wedge, the parity bit now for
+// itself.  After the walk the queue is counted in a small hash (no divergence in the
+// walk) and every repeated end vertex is closed (first wedge from the parity bit), so the
+// adjacency is read once.  A round whose queue overflows is redone narrower.
+struct OpBits {
+  uint32_t bm, queue, count, Q, lo_rank;
+  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
+    const uint32_t rank = w & 0x7fffffffu, rel = rank - lo_rank;
+    const uint32_t neg = (w ^ sg) >> 31;
+    const uint32_t sh = (rel & 15u) << 1;
+    const uint32_t old = s_atom_or(bm + ((rel >> 4) << 2), (1u | (neg << 1)) << sh);
+    if ((old >> sh) & 1u) {
+      const uint32_t cneg = neg & (old >> (sh + 1u));
+      const uint32_t idx = s_atom_add(count, 1u);
+      if (idx < Q) s_st(queue + (idx << 2), rank | (cneg << 31));
+    }
+  }
+  __device__ __forceinline__ void flush() {}
+};
+
+// slot of key (rank + 1) in a linear-probing set of K slots that never fills; bit 31 set
+// when this call inserted it
 __device__ __forceinline__ uint32_t rep_insert(uint32_t* keys, uint32_t K, uint32_t key) {
   volatile uint32_t* vk = keys;
-  uint32_t h = rep_hash(key, K);
+  uint32_t h = (uint32_t)(((unsigned long long)(key * 0x9E3779B1u) * K) >> 32);
   for (;;) {
     uint32_t k = vk[h];
-    if (k == key) return 0u;
+    if (k == key) return h;
     if (k == 0u) {
       k = atomicCAS(&keys[h], 0u, key);
-      if (k == 0u) return 1u;
-      if (k == key) return 0u;
+      if (k == 0u) return h | 0x80000000u;
+      if (k == key) return h;
     }
     h = (h + 1u == K) ? 0u : h + 1u;
-  }
-}
-
-__device__ __forceinline__ int rep_find(const uint32_t* keys, uint32_t K, uint32_t key) {
-  uint32_t h = rep_hash(key, K);
-  for (;;) {
-    const uint32_t k = keys[h];
-    if (k == key) return (int)h;
-    if (k == 0u) return -1;
-    h = (h + 1u == K) ? 0u : h + 1u;
-  }
-}
-
-// PASS 0: mark + collect repeats (insertions counted in *s_ins); PASS 1: exact count.
-template <int T, int PASS>
-__device__ __forceinline__ void walk_cold(const Params& P, uint32_t* bm, uint32_t* keys, uint32_t* vals, uint32_t K,
-                                          const uint32_t* s_lo, const uint32_t* s_hi, const uint32_t* s_pfx, int nb,
-                                          uint32_t ngroups, uint32_t lo_rank, unsigned long long& tb,
-                                          unsigned long long& tu, uint32_t* s_ins) {
-  const uint4* adj4 = reinterpret_cast<const uint4*>(P.adj);
-  const uint32_t limit = K / 2u;
-  for (uint32_t g0 = threadIdx.x; g0 < ngroups; g0 += 2 * T) {
-    uint4 q[2];
-    uint32_t lo[2], hi[2], sg[2], p0[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const uint32_t g = g0 + (uint32_t)i * T;
-      lo[i] = 1u;
-      hi[i] = 0u;
-      sg[i] = 0u;
-      p0[i] = 0u;
-      q[i] = make_uint4(0u, 0u, 0u, 0u);
-      if (g < ngroups) {
-        const int k = find_record(s_pfx, nb, g);
-        const uint32_t lox = s_lo[k];
-        lo[i] = lox & 0x7fffffffu;
-        sg[i] = lox & 0x80000000u;
-        hi[i] = s_hi[k];
-        const uint32_t grp = (lo[i] >> 2) + (g - s_pfx[k]);
-        p0[i] = grp << 2;
-        q[i] = ld_stream(adj4 + grp);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const uint32_t wv[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t p = p0[i] + (uint32_t)j;
-        if (p >= lo[i] && p < hi[i]) {
-          const uint32_t rank = wv[j] & 0x7fffffffu;
-          if (PASS == 0) {
-            const uint32_t rel = rank - lo_rank;
-            const uint32_t bit = 1u << (rel & 31u);
-            const uint32_t old = atomicOr(&bm[rel >> 5], bit);
-            if ((old & bit) && *(volatile uint32_t*)s_ins < limit) {
-              if (rep_insert(keys, K, rank + 1u)) atomicAdd(s_ins, 1u);
-            }
-          } else {
-            const int slot = rep_find(keys, K, rank + 1u);
-            if (slot >= 0) {
-              const uint32_t sh = ((wv[j] ^ sg[i]) >> 31) << 4;
-              const uint32_t old = atomicAdd(&vals[slot], 1u << sh);
-              tb += (old >> sh) & 0xffffu;
-              tu += (old >> (sh ^ 16u)) & 0xffffu;
-            }
-          }
-        }
-      }
-    }
-  }
-}
-
-// Sparse band walk with at most two int4 groups per thread: both loads are issued before
-// either group is processed, and the touched counter words are kept in registers so the
-// zeroing pass needs neither the adjacency nor the record search again.
-template <int T, int W>
-__device__ __forceinline__ void walk2_sparse(const Params& P, uint32_t* cnt, const uint32_t* s_lo,
-                                             const uint32_t* s_hi, const uint32_t* s_pfx, int nb, uint32_t ngroups,
-                                             uint32_t lo_rank, unsigned long long& tb, unsigned long long& tu,
-                                             uint32_t (&touched)[8]) {
-  const uint4* adj4 = reinterpret_cast<const uint4*>(P.adj);
-  uint4 q[2];
-  uint32_t lo[2], hi[2], sg[2], p0[2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const uint32_t g = threadIdx.x + (uint32_t)i * T;
-    lo[i] = 1u;
-    hi[i] = 0u;
-    sg[i] = 0u;
-    p0[i] = 0u;
-    q[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (g < ngroups) {
-      const int k = find_record(s_pfx, nb, g);
-      const uint32_t lox = s_lo[k];
-      lo[i] = lox & 0x7fffffffu;
-      sg[i] = lox & 0x80000000u;
-      hi[i] = s_hi[k];
-      const uint32_t grp = (lo[i] >> 2) + (g - s_pfx[k]);
-      p0[i] = grp << 2;
-      q[i] = ld_stream(adj4 + grp);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const uint32_t wv[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t p = p0[i] + (uint32_t)j;
-      touched[4 * i + j] = 0xffffffffu;
-      if (p >= lo[i] && p < hi[i]) {
-        const uint32_t rel = (wv[j] & 0x7fffffffu) - lo_rank;
-        bump_close<W>(cnt, rel, (wv[j] ^ sg[i]) >> 31, tb, tu);
-        touched[4 * i + j] = W == 8 ? (rel >> 1) : rel;
-      }
-    }
   }
 }
 
@@ -595,39 +604,56 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     uint32_t ngroups;
     const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w);
     if (mine) S.pfx[threadIdx.x] = ex;
+    if ((P.debug & 4096) && threadIdx.x == 0) {
+      atomicAdd(P.acc + 8, (unsigned long long)ngroups);
+      atomicAdd(P.acc + 9, bw);
+      atomicAdd(P.acc + 10, 1ull);
+    }
     __syncthreads();
     return ngroups;
   };
   // one tile round over band columns [ca, ca + cols)
   auto tile_round = [&](uint32_t ca, uint32_t cols, uint32_t ngroups, unsigned long long bw) {
+    if ((P.debug & 4096) && threadIdx.x == 0) atomicAdd(P.acc + 6, 1ull);
     const long long top = (long long)P.n - (long long)ca * t16;
     const long long bot = top - (long long)cols * t16;
     const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
     const uint32_t band_span = (uint32_t)(top - (long long)lo_rank);
     const uint32_t band_words = W == 8 ? (band_span + 1u) / 2u : band_span;
+    const uint32_t base = sptr(S.cnt);
     if (ngroups <= 2u * T) {
-      uint32_t touched[8];
-      walk2_sparse<T, W>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu, touched);
+      // at most one pair of groups per thread: close inline and zero the touched words
+      // from registers (no second pass over the tile or the adjacency)
+      OpTileClose<W, true> op{base, lo_rank, &tb, &tu};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) op.touched[j] = 0xffffffffu;
+      walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (touched[j] != 0xffffffffu) S.cnt[touched[j]] = 0u;
-    } else if (P.debug & 16) {  // (A/B switch) inline closing + global re-walk to zero
-      walk<T, W, kSparse>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
+        if (op.touched[j] != 0xffffffffu) s_st(op.touched[j], 0u);
+    } else if (bw < (unsigned long long)P.sweep_min * band_words && !(P.debug & 2048)) {
+      // medium rounds: inline closing, then the tile is cleared with vector stores (a
+      // closing sweep costs ~9 instructions per counter word, inline closing ~4 per wedge)
+      OpTileClose<W, false> op{base, lo_rank, &tb, &tu};
+      walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
-      walk<T, W, kZero>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
+      uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
+      for (uint32_t i = threadIdx.x; i < (band_words + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
     } else {
-      // more than two groups per thread: no-return increments and the shared-memory
-      // closing sweep, which is cheaper than re-reading the adjacency to zero
-      walk<T, W, kDense>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
+      // dense rounds: no-return increments and the shared-memory closing sweep
+      OpTileDense<W> op{base, lo_rank};
+      walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
       sweep<T, W>(S.cnt, band_words, tb, tu);
     }
     __syncthreads();
   };
   auto hash_round = [&](uint32_t ngroups, unsigned long long bw) {
+    if ((P.debug & 4096) && threadIdx.x == 0) atomicAdd(P.acc + 7, 1ull);
     const uint32_t K = min(P.hslots, max(64u, (uint32_t)(2ull * bw + 31ull) & ~31u));
-    walk_hash<T>(P, S.cnt, K, S.lo, S.hi, S.pfx, nb, ngroups, tb, tu);
+    OpHash op{S.cnt, K, &tb, &tu};
+    walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ngroups, op);
     __syncthreads();
     uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
     for (uint32_t i = threadIdx.x; i < (2u * K + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -660,54 +686,99 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     if (ng) tile_round(0u, hstep, ng, bw);
   }
   if (P.phase == 1 || ncols <= hstep || (P.debug & 8)) return;
-  // cold range in seen-bitmap rounds of bm_cols columns (see walk_cold)
+  // cold range in two-bit bitmap rounds (see OpBits).  A round of `cols` columns uses
+  // cols * t16 / 16 bitmap words and gives the rest of the tile to the repeat queue and
+  // its hash, so narrow rounds tolerate many repeats.  Repeats are densest just below the
+  // hub band (higher-degree end vertices), so rounds start narrow and double while the
+  // queue stays under 1/4 full; an overflowing round is redone at half the width (one
+  // column: a counter tile).
   auto bitmap_rounds = [&]() {
-    uint32_t* bm = S.cnt;
-    uint32_t* keys = S.cnt + P.bm_words;
-    uint32_t* vals = keys + P.rep_slots;
-    const uint32_t K = P.rep_slots;
+    uint32_t cols = P.bm_cols0;
     uint32_t hi = c1;
-    for (uint32_t c = hstep; c < ncols; c += P.bm_cols) {
-      const uint32_t cb = min(c + P.bm_cols, ncols);
+    for (uint32_t c = hstep; c < ncols;) {
+      const uint32_t cb = min(c + cols, ncols);
       const uint32_t lo = col(cb);
       if (t0) *S.ins = 0u;  // published by setup's barriers
       unsigned long long bw;
       const uint32_t ng = setup(hi, lo, bw);
-      if (t0) work += bw;
-      hi = lo;
-      if (ng == 0u) continue;
+      if (ng == 0u) {
+        hi = lo;
+        c = cb;
+        continue;
+      }
       const long long top = (long long)P.n - (long long)c * t16;
       const long long bot = (long long)P.n - (long long)cb * t16;
       const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
-      const uint32_t span_words = (uint32_t)((top - (long long)lo_rank + 31) / 32);
-      walk_cold<T, 0>(P, bm, keys, vals, K, S.lo, S.hi, S.pfx, nb, ng, lo_rank, tb, tu, S.ins);
+      const uint32_t span_words = (uint32_t)((top - (long long)lo_rank + 15) / 16 + 3) & ~3u;
+      // queue of Q repeats, then a 2Q-slot key set and its packed counts (never fills)
+      const uint32_t Q = ((P.cap_words - span_words) / 5u) & ~3u;
+      const uint32_t K = 2u * Q;
+      uint32_t* bm = S.cnt;
+      uint32_t* queue = S.cnt + span_words;
+      uint32_t* keys = queue + Q;
+      uint32_t* vals = keys + K;
+      OpBits op{sptr(bm), sptr(queue), sptr(S.ins), Q, lo_rank};
+      walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ng, op);
       __syncthreads();
-      const bool ovf = *S.ins >= K / 2u;
-      if (!ovf) walk_cold<T, 1>(P, bm, keys, vals, K, S.lo, S.hi, S.pfx, nb, ng, lo_rank, tb, tu, S.ins);
-      __syncthreads();
-      uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
-      for (uint32_t i = threadIdx.x; i < (span_words + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
-      for (uint32_t i = threadIdx.x; i < (2u * K) / 4u; i += T) c4[P.bm_words / 4u + i] = make_uint4(0u, 0u, 0u, 0u);
-      __syncthreads();
-      if (ovf) {
-        // too many repeated end vertices for the set: counter tiles for these columns
-        uint32_t thi = col(c);
-        for (uint32_t cc = c; cc < cb; cc += step) {
-          const uint32_t tlo = col(min(cc + step, cb));
-          unsigned long long tbw;
-          const uint32_t tng = setup(thi, tlo, tbw);
-          if (tng) tile_round(cc, step, tng, tbw);
-          thi = tlo;
+      const uint32_t nq = *S.ins;
+      const bool ovf = nq > Q;
+      if (!ovf) {
+        // count the repeats per end vertex; the inserting entry is kept as the closer
+        for (uint32_t i = threadIdx.x; i < nq; i += T) {
+          const uint32_t e = queue[i];
+          const uint32_t h = rep_insert(keys, K, (e & 0x7fffffffu) + 1u);
+          atomicAdd(&vals[h & 0x7fffffffu], (e >> 31) ? 0x10000u : 1u);
+          queue[i] = (h >> 31) ? h : 0u;
         }
+        __syncthreads();
+        // close every repeated end vertex: first wedge from the parity bit + the counts
+        for (uint32_t i = threadIdx.x; i < nq; i += T) {
+          const uint32_t e = queue[i];
+          if (e == 0u) continue;
+          const uint32_t h = e & 0x7fffffffu;
+          const uint32_t rel = keys[h] - 1u - lo_rank;
+          const uint32_t neg = (bm[rel >> 4] >> (((rel & 15u) << 1) + 1u)) & 1u;
+          const uint32_t v = vals[h];
+          const unsigned long long pc = (v & 0xffffu) + (neg ^ 1u), qc = (v >> 16) + neg;
+          tb += ((pc * (pc - 1ull)) >> 1) + ((qc * (qc - 1ull)) >> 1);
+          tu += pc * qc;
+          keys[h] = 0u;
+          vals[h] = 0u;
+          queue[i] = 0u;
+        }
+      } else {
+        uint4* q4 = reinterpret_cast<uint4*>(queue);
+        for (uint32_t i = threadIdx.x; i < Q / 4u; i += T) q4[i] = make_uint4(0u, 0u, 0u, 0u);
+      }
+      __syncthreads();
+      uint4* c4 = reinterpret_cast<uint4*>(bm);
+      for (uint32_t i = threadIdx.x; i < span_words / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+      if (P.debug & 4096) {
+        if (t0) atomicAdd(P.acc + 4, 1ull);
+        if (t0 && ovf) atomicAdd(P.acc + 5, 1ull);
+      }
+      if (!ovf) {
+        if (t0) work += bw;
+        hi = lo;
+        c = cb;
+        if (nq < Q / 4u) cols = min(2u * cols, P.bm_cols);
+      } else if (cols > 1u) {
+        cols = (cols + 1u) / 2u;  // redo [c, c + cols) (the zeroing is ordered by setup's barriers)
+      } else {
+        // a single column with too many repeats: one counter-tile round
+        unsigned long long tbw;
+        const uint32_t tng = setup(hi, lo, tbw);
+        if (t0) work += tbw;
+        if (tng) tile_round(c, 1u, tng, tbw);
+        hi = lo;
+        c = cb;
       }
     }
   };
 
-  // cold range: one hash round if it fits; else seen-bitmap rounds when counter tiles
-  // would average fewer than 64 wedges per round (very wide, sparse end-vertex ranges,
-  // e.g. tens of millions of ranks); else counter tiles band by band.  (A single
-  // hashed-filter round for medium anchors was measured slower than tiles: probe
-  // divergence and two passes.)
+  // cold range: one hash round if it fits; else two-bit bitmap rounds (8x the span of a
+  // counter tile) unless counter tiles would average at least bits_thr wedges per round
+  // (dense cold ranges, where repeats are common); else counter tiles band by band.
   if (P.hslots != 0u || P.bm_cols != 0u) {
     unsigned long long wc;
     const uint32_t ng = setup(c1, cn, wc);
@@ -717,7 +788,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       return;
     }
     const unsigned long long tile_rounds = (ncols - hstep + step - 1u) / step;
-    if (P.bm_cols != 0u && (wc < 64ull * tile_rounds || (P.debug & 512))) {  // 512: force (tests)
+    if (P.bm_cols != 0u && (wc < (unsigned long long)P.bits_thr * tile_rounds || (P.debug & 512))) {
       bitmap_rounds();
       return;
     }
@@ -912,6 +983,15 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
   const uint32_t ntasks =
       n > (uint32_t)opts.part_index ? (n - (uint32_t)opts.part_index + part_count - 1) / part_count : 0u;
 
+  // tuning knobs (defaults measured on config 2; env overrides for experiments)
+  struct {
+    uint32_t rep_slots = 256, bits_thr = 4096, sweep_min = 2, bm_cols0 = 2;
+  } tune;
+  if (const char* e = std::getenv("BBC_BM_COLS0")) tune.bm_cols0 = (uint32_t)std::atoi(e);
+  if (const char* e = std::getenv("BBC_REP_SLOTS")) tune.rep_slots = (uint32_t)std::atoi(e);
+  if (const char* e = std::getenv("BBC_BITS_THR")) tune.bits_thr = (uint32_t)std::atoi(e);
+  if (const char* e = std::getenv("BBC_SWEEP_MIN")) tune.sweep_min = (uint32_t)std::atoi(e);
+
   auto params = [&](const Launch& X, int phase) {
     Params P;
     uint32_t span16 = (uint32_t)X.cap_words - 8u;
@@ -948,10 +1028,16 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     P.fast = ((opts.flags & 1) || tile_override || g.t16 == 0) ? 0 : 1;
     P.fast_max = two_phase ? (uint32_t)std::min(L.threads, Lc.threads) : (uint32_t)X.threads;
     P.hslots = (opts.flags & 2) ? 0u : (uint32_t)X.cap_words / 2u;
-    // cold seen-bitmap rounds (flags bit 7 disables): 1/8 of the tile for the repeat set
-    P.rep_slots = std::max(64u, ((uint32_t)X.cap_words / (P.debug & 256 ? 4u : 16u)) & ~3u);
-    P.bm_words = ((uint32_t)X.cap_words - 2u * P.rep_slots) & ~3u;
-    P.bm_cols = (opts.flags & 128) ? 0u : (32u * P.bm_words) / std::max(1u, g.t16);
+    // cold two-bit bitmap rounds (flags bit 7 disables): the widest round leaves room for
+    // a queue of rep_slots repeats (flags bit 8: 16, and rounds start at that width, so
+    // that tests exercise the overflow / narrowing path)
+    const uint32_t rep = (opts.flags & 256) ? 16u : tune.rep_slots;
+    P.rep_slots = std::max(16u, std::min(rep, (uint32_t)X.cap_words / 10u) & ~3u);
+    P.bm_words = ((uint32_t)X.cap_words - 5u * P.rep_slots) & ~3u;
+    P.bm_cols = (opts.flags & 128) ? 0u : (16u * P.bm_words) / std::max(1u, g.t16);
+    P.bm_cols0 = std::max(1u, std::min(P.bm_cols, (opts.flags & 256) ? P.bm_cols : tune.bm_cols0));
+    P.bits_thr = tune.bits_thr;
+    P.sweep_min = tune.sweep_min;
     P.debug = opts.flags;
     P.dynamic = opts.algo == BBC_ALGO_GBBCPP;
     P.acc = g.acc;
@@ -960,7 +1046,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     return P;
   };
 
-  BBC_CK(cudaMemsetAsync(g.acc, 0, 32, g.stream));
+  BBC_CK(cudaMemsetAsync(g.acc, 0, 128, g.stream));
   BBC_CK(cudaMemsetAsync(g.queue, 0, 8, g.stream));
   BBC_CK(cudaMemsetAsync(g.block_work, 0, (size_t)blocks * 8, g.stream));
   BBC_CK(cudaEventRecord(g.ev0, g.stream));
@@ -974,12 +1060,13 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
   }
   BBC_CK(cudaEventRecord(g.ev1, g.stream));
   const uint32_t span16 = P1.span16;
-  unsigned long long h_acc[4];
-  BBC_CK(cudaMemcpyAsync(h_acc, g.acc, 32, cudaMemcpyDeviceToHost, g.stream));
+  unsigned long long h_acc[16];
+  BBC_CK(cudaMemcpyAsync(h_acc, g.acc, 128, cudaMemcpyDeviceToHost, g.stream));
   BBC_CK(cudaStreamSynchronize(g.stream));
   g.last_blocks = blocks;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, g.ev0, g.ev1);
+  for (int i = 0; i < 8; ++i) g.rounds[i] = h_acc[4 + i];
   out[0] = h_acc[0];
   out[1] = h_acc[2];
   if (st) {

@@ -50,6 +50,8 @@ struct Graph {
   unsigned long long* block_work = nullptr; // [block_work_cap]
   int block_work_cap = 0;
   int last_blocks = 0;
+  uint64_t rounds[8] = {};  // last count with flags bit 12: bitmap, overflowed, tile, hash rounds;
+                           // walked groups, walked wedges, round setups
   int num_sms = 0;
   int max_smem = 0;
   int threads = 128;  // count-kernel CTA size (128 / 256 / 512 / 1024; env BBC_THREADS)

@@ -477,7 +477,7 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
     }
   }
 
-  BBC_ALLOC(g.acc, 64);
+  BBC_ALLOC(g.acc, 128);
   BBC_ALLOC(g.queue, 64);
   g.block_work_cap = std::max(1, sms * 32);
   BBC_ALLOC(g.block_work, (size_t)g.block_work_cap * 8);

@@ -21,3 +21,5 @@ for _ in range(a.reps):
     r = g.count(a.algo, a.tile, flags=a.flags)
     print(f"{cfg.name}: balanced={r.balanced} unbalanced={r.unbalanced} W={r.wedges} count_ms={r.count_ms:.3f} "
           f"prep_ms={r.preprocess_ms:.3f} rate={r.wedges / r.count_ms * 1e3:.3e}/s", flush=True)
+if a.flags & _lib.FLAG_ROUNDS:
+    print("rounds", g.round_counters(), flush=True)
