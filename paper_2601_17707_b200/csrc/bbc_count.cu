@@ -59,7 +59,7 @@ struct Params {
   uint32_t span32;
   uint32_t cap_words;
   int fast;         // 0: always the general banded path (flags bit 0)
-  uint32_t hslots;  // cold-range hash slots (0: band by band; flags bit 1)
+  uint32_t hslots;  // cold-range hash slots (0: no hash round; flags bit 13 enables)
   uint32_t t16;     // band-table granularity (ranks per column)
   uint32_t bcols8;  // this launch's tile band in table columns (W8 / W16 layouts)
   uint32_t bcols16;
@@ -254,7 +254,13 @@ __device__ __forceinline__ void hash_bump_close(uint32_t* tab, uint32_t K, uint3
 
 // ---- shared-memory primitives on 32-bit shared addresses ------------------------------
 // (generic pointers make the compiler re-derive the shared window base per access)
-__device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// (the move is opaque to the compiler, so a base address stays in one register instead of
+// being re-derived from the CTA's shared window before every atomic)
+__device__ __forceinline__ uint32_t sptr(const void* p) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(a));
+  return r;
+}
 __device__ __forceinline__ uint32_t s_atom_add(uint32_t a, uint32_t v) {
   uint32_t r;
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
@@ -316,16 +322,21 @@ __device__ __forceinline__ void walk_pairs(const Params& P, const uint32_t* s_lo
   }
 }
 
+// The tile / bitmap ops address their words from a REBASED shared address: rb = base -
+// (lo_rank / ranks-per-word) * 4 (mod 2^32), so a wedge's word is rb + (rank / per-word) * 4
+// with no subtraction; lo_rank is aligned to the ranks per word (tiles are sized with the
+// slack).  Ranks are < 2^30 on the fast path, so (w >> s) keeps no sign bit after masking.
+
 // counter-tile increments without return (closed later by the sweep)
 template <int W>
 struct OpTileDense {
-  uint32_t base, lo_rank;
+  uint32_t rb;
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
-    const uint32_t rel = (w & 0x7fffffffu) - lo_rank, par = (w ^ sg) >> 31;
+    const uint32_t v = w ^ sg;  // bit 31: parity (1 = negative wedge)
     if (W == 8)
-      s_red_add(base + ((rel >> 1) << 2), 1u << (((rel & 1u) << 4) | (par << 3)));
+      s_red_add(rb + ((w << 1) & 0xfffffffcu), 1u << (((w & 1u) << 4) | ((v >> 28) & 8u)));
     else
-      s_red_add(base + (rel << 2), 1u << (par << 4));
+      s_red_add(rb + ((w << 2) & 0xfffffffcu), 1u << ((v >> 27) & 16u));
   }
   __device__ __forceinline__ void flush() {}
 };
@@ -336,22 +347,22 @@ struct OpTileDense {
 // KEEP the touched word of each slot is kept (single-iteration rounds zero from it).
 template <int W, bool KEEP>
 struct OpTileClose {
-  uint32_t base, lo_rank;
+  uint32_t rb;
   unsigned long long *tb, *tu;
   uint32_t b32 = 0, u32 = 0;
   uint32_t touched[8];
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int j) {
-    const uint32_t rel = (w & 0x7fffffffu) - lo_rank, par = (w ^ sg) >> 31;
+    const uint32_t v = w ^ sg;
     if (W == 8) {
-      const uint32_t sh = ((rel & 1u) << 4) | (par << 3);
-      const uint32_t a = base + ((rel >> 1) << 2);
+      const uint32_t sh = ((w & 1u) << 4) | ((v >> 28) & 8u);
+      const uint32_t a = rb + ((w << 1) & 0xfffffffcu);
       const uint32_t old = s_atom_add(a, 1u << sh);
       b32 += (old >> sh) & 0xffu;
       u32 += (old >> (sh ^ 8u)) & 0xffu;
       if (KEEP) touched[j] = a;
     } else {
-      const uint32_t sh = par << 4;
-      const uint32_t a = base + (rel << 2);
+      const uint32_t sh = (v >> 27) & 16u;
+      const uint32_t a = rb + ((w << 2) & 0xfffffffcu);
       const uint32_t old = s_atom_add(a, 1u << sh);
       b32 += (old >> sh) & 0xffffu;
       u32 += (old >> (sh ^ 16u)) & 0xffffu;
@@ -380,8 +391,8 @@ struct OpHash {
 // In the cold end-vertex range almost every (anchor, end vertex) pair has one common
 // centre (config 2: 2.7 % of the cold wedges land on a repeated end vertex), and a pair
 // with one wedge contributes nothing.  A cold round therefore keeps two bits per end
-// vertex (8x denser than a u8x2 counter tile, so one round spans 8x more ranks):
-//   bit 0: seen;  bit 1: parity (1 = negative) of the FIRST wedge.
+// vertex (8x denser than a u8x2 counter tile, so one round spans 8x more ranks): word
+// bit i = seen, bit 16 + i = parity (1 = negative) of the FIRST wedge, for 16 end vertices.
 // Every wedge ORs in its seen bit and, when negative, the parity bit, in ONE atomic.  A
 // wedge that finds the seen bit already set is a repeat and is appended to a queue as
 // (rank, counted parity): a negative repeat that turned the parity bit from 0 to 1 is
@@ -390,16 +401,15 @@ struct OpHash {
 // walk) and every repeated end vertex is closed (first wedge from the parity bit), so the
 // adjacency is read once.  A round whose queue overflows is redone narrower.
 struct OpBits {
-  uint32_t bm, queue, count, Q, lo_rank;
+  uint32_t rb, queue, count, Q;
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
-    const uint32_t rank = w & 0x7fffffffu, rel = rank - lo_rank;
-    const uint32_t neg = (w ^ sg) >> 31;
-    const uint32_t sh = (rel & 15u) << 1;
-    const uint32_t old = s_atom_or(bm + ((rel >> 4) << 2), (1u | (neg << 1)) << sh);
-    if ((old >> sh) & 1u) {
-      const uint32_t cneg = neg & (old >> (sh + 1u));
+    const uint32_t i = w & 15u;                     // bit i: seen, bit 16 + i: parity
+    const uint32_t v = w ^ sg;
+    const uint32_t old = s_atom_or(rb + ((w >> 2) & 0x0ffffffcu), (((v >> 15) & 0x10000u) | 1u) << i);
+    if ((old >> i) & 1u) {
+      const uint32_t cneg = (v >> 31) & (old >> (16u + i));
       const uint32_t idx = s_atom_add(count, 1u);
-      if (idx < Q) s_st(queue + (idx << 2), rank | (cneg << 31));
+      if (idx < Q) s_st(queue + (idx << 2), (w & 0x7fffffffu) | (cneg << 31));
     }
   }
   __device__ __forceinline__ void flush() {}
@@ -617,14 +627,15 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     if ((P.debug & 4096) && threadIdx.x == 0) atomicAdd(P.acc + 6, 1ull);
     const long long top = (long long)P.n - (long long)ca * t16;
     const long long bot = top - (long long)cols * t16;
-    const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
+    // lo_rank aligned to the ranks per word (W8: 2), see the rebased ops
+    const uint32_t lo_rank = (bot > 0 ? (uint32_t)bot : 0u) & (W == 8 ? ~1u : ~0u);
     const uint32_t band_span = (uint32_t)(top - (long long)lo_rank);
     const uint32_t band_words = W == 8 ? (band_span + 1u) / 2u : band_span;
-    const uint32_t base = sptr(S.cnt);
+    const uint32_t base = sptr(S.cnt) - (W == 8 ? (lo_rank >> 1) << 2 : lo_rank << 2);
     if (ngroups <= 2u * T) {
       // at most one pair of groups per thread: close inline and zero the touched words
       // from registers (no second pass over the tile or the adjacency)
-      OpTileClose<W, true> op{base, lo_rank, &tb, &tu};
+      OpTileClose<W, true> op{base, &tb, &tu};
 #pragma unroll
       for (int j = 0; j < 8; ++j) op.touched[j] = 0xffffffffu;
       walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ngroups, op);
@@ -635,14 +646,14 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     } else if (bw < (unsigned long long)P.sweep_min * band_words && !(P.debug & 2048)) {
       // medium rounds: inline closing, then the tile is cleared with vector stores (a
       // closing sweep costs ~9 instructions per counter word, inline closing ~4 per wedge)
-      OpTileClose<W, false> op{base, lo_rank, &tb, &tu};
+      OpTileClose<W, false> op{base, &tb, &tu};
       walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
       uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
       for (uint32_t i = threadIdx.x; i < (band_words + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
     } else {
       // dense rounds: no-return increments and the shared-memory closing sweep
-      OpTileDense<W> op{base, lo_rank};
+      OpTileDense<W> op{base};
       walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
       sweep<T, W>(S.cnt, band_words, tb, tu);
@@ -708,7 +719,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       }
       const long long top = (long long)P.n - (long long)c * t16;
       const long long bot = (long long)P.n - (long long)cb * t16;
-      const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
+      const uint32_t lo_rank = (bot > 0 ? (uint32_t)bot : 0u) & ~15u;  // rebased ops: 16 per word
       const uint32_t span_words = (uint32_t)((top - (long long)lo_rank + 15) / 16 + 3) & ~3u;
       // queue of Q repeats, then a 2Q-slot key set and its packed counts (never fills)
       const uint32_t Q = ((P.cap_words - span_words) / 5u) & ~3u;
@@ -717,7 +728,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       uint32_t* queue = S.cnt + span_words;
       uint32_t* keys = queue + Q;
       uint32_t* vals = keys + K;
-      OpBits op{sptr(bm), sptr(queue), sptr(S.ins), Q, lo_rank};
+      OpBits op{sptr(bm) - ((lo_rank >> 4) << 2), sptr(queue), sptr(S.ins), Q};
       walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ng, op);
       __syncthreads();
       const uint32_t nq = *S.ins;
@@ -737,7 +748,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
           if (e == 0u) continue;
           const uint32_t h = e & 0x7fffffffu;
           const uint32_t rel = keys[h] - 1u - lo_rank;
-          const uint32_t neg = (bm[rel >> 4] >> (((rel & 15u) << 1) + 1u)) & 1u;
+          const uint32_t neg = (bm[rel >> 4] >> (16u + (rel & 15u))) & 1u;
           const uint32_t v = vals[h];
           const unsigned long long pc = (v & 0xffffu) + (neg ^ 1u), qc = (v >> 16) + neg;
           tb += ((pc * (pc - 1ull)) >> 1) + ((qc * (qc - 1ull)) >> 1);
@@ -985,7 +996,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
 
   // tuning knobs (defaults measured on config 2; env overrides for experiments)
   struct {
-    uint32_t rep_slots = 256, bits_thr = 4096, sweep_min = 2, bm_cols0 = 2;
+    uint32_t rep_slots = 256, bits_thr = 4096, sweep_min = 2, bm_cols0 = 4;
   } tune;
   if (const char* e = std::getenv("BBC_BM_COLS0")) tune.bm_cols0 = (uint32_t)std::atoi(e);
   if (const char* e = std::getenv("BBC_REP_SLOTS")) tune.rep_slots = (uint32_t)std::atoi(e);
@@ -1024,10 +1035,13 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     P.span16 = span16;
     P.span32 = span32;
     P.cap_words = (uint32_t)X.cap_words;
-    // the fast path needs the fixed column grid: not with TileConfig.tile_size spans
-    P.fast = ((opts.flags & 1) || tile_override || g.t16 == 0) ? 0 : 1;
+    // the fast path needs the fixed column grid (not with TileConfig.tile_size spans) and
+    // ranks < 2^30 (rebased word addressing)
+    P.fast = ((opts.flags & 1) || tile_override || g.t16 == 0 || n >= (1u << 30)) ? 0 : 1;
     P.fast_max = two_phase ? (uint32_t)std::min(L.threads, Lc.threads) : (uint32_t)X.threads;
-    P.hslots = (opts.flags & 2) ? 0u : (uint32_t)X.cap_words / 2u;
+    // one-round cold hash for light anchors: flags bit 13 (measured slower than bitmap
+    // rounds on config 2 once those had a repeat queue: 17.0 vs 16.4 ms)
+    P.hslots = (opts.flags & 8192) && !(opts.flags & 2) ? (uint32_t)X.cap_words / 2u : 0u;
     // cold two-bit bitmap rounds (flags bit 7 disables): the widest round leaves room for
     // a queue of rep_slots repeats (flags bit 8: 16, and rounds start at that width, so
     // that tests exercise the overflow / narrowing path)

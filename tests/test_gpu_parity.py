@@ -71,10 +71,12 @@ def test_synthetic_configs_vs_reference(gpu, golden, key):
     for side in (SIDE_CHEAPER, SIDE_U, SIDE_V):
         for algo in ALGOS:
             g = DeviceGraph.from_host(cfg.n_u, cfg.n_v, u, v, s, 0, side)
-            # every cold-range strategy: default, general banded path, no hash, forced
-            # seen-bitmap rounds (small / large repeat set), tiles only, two launches
+            # every cold-range strategy: default, general banded path, hash rounds (8192),
+            # forced bitmap rounds (normal / tiny repeat queue: overflow + narrowing),
+            # tiles only (128), sweep-closed tiles (2048), two launches (64)
             # (1024: band boundaries by binary search instead of the table)
-            for flags in (0, _lib.FLAG_BANDED_ONLY, 2, 2 | 512, 2 | 512 | 256, 2 | 128, 64, 1024, 1024 | 2 | 512):
+            for flags in (0, _lib.FLAG_BANDED_ONLY, 8192, 512, 512 | 256, 128, 128 | 2048, 64, 1024, 1024 | 512,
+                          1024 | 8192):
                 r = g.count(algo, flags=flags)
                 assert (r.balanced, r.unbalanced) == (rec["balanced"], rec["unbalanced"]), (key, side, algo, flags)
                 assert r.wedges == r.wedges_total == (rec["w_u"] if g.anchor_side == 0 else rec["w_v"])
