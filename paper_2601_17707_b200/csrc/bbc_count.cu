@@ -100,10 +100,14 @@ __device__ __forceinline__ uint32_t lower_bound_rank(const uint32_t* __restrict_
   return lo;
 }
 
-// Block-wide exclusive scan of one u32 per thread fused with a u64 sum.
+// Block-wide exclusive scan of one u32 per thread fused with a u64 sum, with ONE barrier:
+// each warp publishes its totals, then every warp scans the (<= 32) warp totals itself.
+// The totals are double-buffered by `buf` (callers alternate it), since consecutive scans
+// may have no other barrier between them and a warp can be one scan ahead.
 template <int T>
 __device__ __forceinline__ uint32_t scan_sum(uint32_t v, unsigned long long w, uint32_t& total,
-                                             unsigned long long& wtotal, uint32_t* s_v, unsigned long long* s_w) {
+                                             unsigned long long& wtotal, uint32_t* s_v, unsigned long long* s_w,
+                                             uint32_t buf) {
   constexpr int kWarps = T / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t x = v;
@@ -114,26 +118,24 @@ __device__ __forceinline__ uint32_t scan_sum(uint32_t v, unsigned long long w, u
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(kFull, w, o);
-  if (lane == 31) s_v[warp] = x;
-  if (lane == 0) s_w[warp] = w;
+  uint32_t* sv = s_v + (buf & 1u) * 32u;
+  unsigned long long* sw = s_w + (buf & 1u) * 32u;
+  if (lane == 31) sv[warp] = x;
+  if (lane == 0) sw[warp] = w;
   __syncthreads();
-  if (warp == 0) {
-    uint32_t a = lane < kWarps ? s_v[lane] : 0u;
-    unsigned long long b = lane < kWarps ? s_w[lane] : 0ull;
+  uint32_t a = lane < kWarps ? sv[lane] : 0u;
+  unsigned long long bsum = lane < kWarps ? sw[lane] : 0ull;
 #pragma unroll
-    for (int o = 1; o < kWarps; o <<= 1) {
-      uint32_t y = __shfl_up_sync(kFull, a, o);
-      if (lane >= o) a += y;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(kFull, b, o);
-    if (lane < kWarps) s_v[lane] = a;
-    if (lane == 0) s_w[32] = b;
+  for (int o = 1; o < kWarps; o <<= 1) {
+    uint32_t y = __shfl_up_sync(kFull, a, o);
+    if (lane >= o) a += y;
   }
-  __syncthreads();
-  total = s_v[kWarps - 1];
-  wtotal = s_w[32];
-  return x - v + (warp > 0 ? s_v[warp - 1] : 0u);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) bsum += __shfl_xor_sync(kFull, bsum, o);
+  total = __shfl_sync(kFull, a, kWarps - 1);
+  wtotal = bsum;
+  const uint32_t before = __shfl_sync(kFull, a, (warp + 31) & 31);  // inclusive prefix of warp - 1
+  return x - v + (warp > 0 ? before : 0u);
 }
 
 // largest k in [0, nb) with pfx[k] <= g
@@ -489,6 +491,7 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
   const bool table = P.bnd != nullptr && W != 32;
   const uint32_t nbands_u = (P.n - 1u - r) / span + 1u;  // bands 0..nbands_u-1 hold ranks > r
   const bool multi = (re - rb) > (uint32_t)T;
+  uint32_t scan_buf = 0;  // alternates the scan's total buffers
   for (uint32_t b = 0; b < nbands_u; ++b) {
     const long long top = (long long)P.n - (long long)b * span;
     const long long bot = top - (long long)span;
@@ -527,7 +530,7 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
       }
       uint32_t ngroups;
       unsigned long long bw;
-      const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w);
+      const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w, scan_buf++);
       if ((int)threadIdx.x < nb) S.pfx[threadIdx.x] = ex;
       __syncthreads();
       work += myw;
@@ -563,7 +566,8 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
 // Records stay in registers across rounds.
 template <int T, int W>
 __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, uint32_t rb, uint32_t re,
-                                    unsigned long long& tb, unsigned long long& tu, unsigned long long& work) {
+                                    unsigned long long w_a, unsigned long long& tb, unsigned long long& tu,
+                                    unsigned long long& work) {
   const uint32_t step = W == 8 ? P.bcols8 : P.bcols16;     // this launch's tile band: columns
   // hub band: the phase-1 tile (128 x 8 configuration = table granularity), or this
   // launch's tile when one launch does every band
@@ -572,6 +576,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   const uint32_t ncols = min(P.nbands, (P.n - 1u - r) / t16 + 1u);  // columns holding ranks > r
   const int nb = (int)(re - rb);
   const bool mine = (int)threadIdx.x < nb;
+  uint32_t scan_buf = 0;  // alternates the scan's total buffers
   uint32_t recx = 0u, lend = 0u;
   const uint32_t* row = nullptr;
   if (mine) {
@@ -595,7 +600,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   // columns needed up front are loaded together (one latency)
   const uint32_t c0 = P.phase == 2 ? 0u : col(0u), c1 = col(hstep);
   const uint32_t c2 = P.phase == 1 ? 0u : col(min(hstep + step, ncols));
-  const uint32_t cn = P.phase == 1 ? 0u : col(ncols);
+  const uint32_t cn = (P.phase == 1 || !(P.hslots || (P.debug & 4))) ? 0u : col(ncols);
   // sub-slices [lo, hi) (positions of two table columns) -> S arrays, block scan;
   // returns total groups, bw = total wedges
   auto setup = [&](uint32_t hi, uint32_t lo, unsigned long long& bw) -> uint32_t {
@@ -612,7 +617,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       S.hi[threadIdx.x] = hi;
     }
     uint32_t ngroups;
-    const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w);
+    const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w, scan_buf++);
     if (mine) S.pfx[threadIdx.x] = ex;
     if ((P.debug & 4096) && threadIdx.x == 0) {
       atomicAdd(P.acc + 8, (unsigned long long)ngroups);
@@ -658,7 +663,8 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       __syncthreads();
       sweep<T, W>(S.cnt, band_words, tb, tu);
     }
-    __syncthreads();
+    // no trailing barrier: every caller's next tile use comes after a setup (two barriers)
+    // or after the end of the anchor (one barrier)
   };
   auto hash_round = [&](uint32_t ngroups, unsigned long long bw) {
     if ((P.debug & 4096) && threadIdx.x == 0) atomicAdd(P.acc + 7, 1ull);
@@ -690,11 +696,11 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   };
 
   // the hub band
+  unsigned long long hub_w = 0;
   if (P.phase != 2 && !(P.debug & 4)) {
-    unsigned long long bw;
-    const uint32_t ng = setup(c0, c1, bw);
-    if (t0) work += bw;
-    if (ng) tile_round(0u, hstep, ng, bw);
+    const uint32_t ng = setup(c0, c1, hub_w);
+    if (t0) work += hub_w;
+    if (ng) tile_round(0u, hstep, ng, hub_w);
   }
   if (P.phase == 1 || ncols <= hstep || (P.debug & 8)) return;
   // cold range in two-bit bitmap rounds (see OpBits).  A round of `cols` columns uses
@@ -706,10 +712,12 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   auto bitmap_rounds = [&]() {
     uint32_t cols = P.bm_cols0;
     uint32_t hi = c1;
+    uint32_t parity = 0;  // the queue counter of a round alternates between S.ins[0] / [1]
     for (uint32_t c = hstep; c < ncols;) {
       const uint32_t cb = min(c + cols, ncols);
       const uint32_t lo = col(cb);
-      if (t0) *S.ins = 0u;  // published by setup's barriers
+      uint32_t* cnt = S.ins + (parity++ & 1u);
+      if (t0) *cnt = 0u;  // its last reader finished before the previous round's barriers
       unsigned long long bw;
       const uint32_t ng = setup(hi, lo, bw);
       if (ng == 0u) {
@@ -728,27 +736,29 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       uint32_t* queue = S.cnt + span_words;
       uint32_t* keys = queue + Q;
       uint32_t* vals = keys + K;
-      OpBits op{sptr(bm) - ((lo_rank >> 4) << 2), sptr(queue), sptr(S.ins), Q};
+      OpBits op{sptr(bm) - ((lo_rank >> 4) << 2), sptr(queue), sptr(cnt), Q};
       walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ng, op);
       __syncthreads();
-      const uint32_t nq = *S.ins;
+      const uint32_t nq = *cnt;
       const bool ovf = nq > Q;
-      if (!ovf) {
-        // count the repeats per end vertex; the inserting entry is kept as the closer
+      if (nq != 0u && !ovf) {
+        // count the repeats per end vertex; the inserting entry becomes the closer and
+        // carries the parity bit of the end vertex's first wedge
         for (uint32_t i = threadIdx.x; i < nq; i += T) {
           const uint32_t e = queue[i];
-          const uint32_t h = rep_insert(keys, K, (e & 0x7fffffffu) + 1u);
+          const uint32_t rank = e & 0x7fffffffu;
+          const uint32_t h = rep_insert(keys, K, rank + 1u);
           atomicAdd(&vals[h & 0x7fffffffu], (e >> 31) ? 0x10000u : 1u);
-          queue[i] = (h >> 31) ? h : 0u;
+          const uint32_t rel = rank - lo_rank;
+          const uint32_t neg = (bm[rel >> 4] >> (16u + (rel & 15u))) & 1u;
+          queue[i] = (h >> 31) ? (h | (neg << 30)) : 0u;
         }
         __syncthreads();
-        // close every repeated end vertex: first wedge from the parity bit + the counts
+        // close every repeated end vertex (first wedge from the parity bit + the counts)
         for (uint32_t i = threadIdx.x; i < nq; i += T) {
           const uint32_t e = queue[i];
           if (e == 0u) continue;
-          const uint32_t h = e & 0x7fffffffu;
-          const uint32_t rel = keys[h] - 1u - lo_rank;
-          const uint32_t neg = (bm[rel >> 4] >> (16u + (rel & 15u))) & 1u;
+          const uint32_t h = e & 0x3fffffffu, neg = (e >> 30) & 1u;
           const uint32_t v = vals[h];
           const unsigned long long pc = (v & 0xffffu) + (neg ^ 1u), qc = (v >> 16) + neg;
           tb += ((pc * (pc - 1ull)) >> 1) + ((qc * (qc - 1ull)) >> 1);
@@ -757,11 +767,12 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
           vals[h] = 0u;
           queue[i] = 0u;
         }
-      } else {
+      } else if (ovf) {
         uint4* q4 = reinterpret_cast<uint4*>(queue);
         for (uint32_t i = threadIdx.x; i < Q / 4u; i += T) q4[i] = make_uint4(0u, 0u, 0u, 0u);
       }
-      __syncthreads();
+      // the bitmap is no longer read (closing uses the queue's parity bits); the next
+      // round's setup barriers order this clearing before its walk
       uint4* c4 = reinterpret_cast<uint4*>(bm);
       for (uint32_t i = threadIdx.x; i < span_words / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
       if (P.debug & 4096) {
@@ -774,7 +785,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
         c = cb;
         if (nq < Q / 4u) cols = min(2u * cols, P.bm_cols);
       } else if (cols > 1u) {
-        cols = (cols + 1u) / 2u;  // redo [c, c + cols) (the zeroing is ordered by setup's barriers)
+        cols = (cols + 1u) / 2u;  // redo [c, c + cols)
       } else {
         // a single column with too many repeats: one counter-tile round
         unsigned long long tbw;
@@ -791,8 +802,11 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   // counter tile) unless counter tiles would average at least bits_thr wedges per round
   // (dense cold ranges, where repeats are common); else counter tiles band by band.
   if (P.hslots != 0u || P.bm_cols != 0u) {
-    unsigned long long wc;
-    const uint32_t ng = setup(c1, cn, wc);
+    // cold wedges: the anchor's work minus the hub band's (a block scan only when the hub
+    // round was skipped or a hash round may need the slices)
+    unsigned long long wc = w_a - hub_w;
+    uint32_t ng = 0;
+    if (P.hslots != 0u || (P.debug & 4)) ng = setup(c1, cn, wc);
     if (P.hslots != 0u && 3ull * wc <= 2ull * P.hslots) {  // load <= 2/3
       if (t0) work += wc;
       if (ng) hash_round(ng, wc);
@@ -811,10 +825,10 @@ template <int T, int MINB>
 __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
   constexpr int kWarps = T / 32;
   extern __shared__ uint4 smem4[];
-  __shared__ uint32_t s_v[32];
-  __shared__ unsigned long long s_w[33];
+  __shared__ uint32_t s_v[64];
+  __shared__ unsigned long long s_w[64];
   __shared__ uint32_t s_task;
-  __shared__ uint32_t s_ins;
+  __shared__ uint32_t s_ins[2];
   Smem S;
   S.cnt = reinterpret_cast<uint32_t*>(smem4);
   S.lo = S.cnt + P.cap_words;
@@ -822,7 +836,7 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
   S.pfx = S.hi + T;
   S.v = s_v;
   S.w = s_w;
-  S.ins = &s_ins;
+  S.ins = s_ins;
 
   for (uint32_t i = threadIdx.x; i < P.cap_words / 4; i += T) smem4[i] = make_uint4(0u, 0u, 0u, 0u);
 
@@ -855,9 +869,9 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
       continue;
     }
     if (fast && deg <= 255u)
-      process_anchor_fast<T, 8>(P, S, r, rb, re, tb, tu, work);
+      process_anchor_fast<T, 8>(P, S, r, rb, re, w_a, tb, tu, work);
     else if (fast)
-      process_anchor_fast<T, 16>(P, S, r, rb, re, tb, tu, work);
+      process_anchor_fast<T, 16>(P, S, r, rb, re, w_a, tb, tu, work);
     else if (deg <= 255u)
       process_anchor<T, 8>(P, S, r, rb, re, tb, tu, work);
     else if (deg <= 65535u)
