@@ -151,6 +151,19 @@ __device__ __forceinline__ int find_record(const uint32_t* pfx, int nb, uint32_t
   return lo;
 }
 
+// the same for nb <= N (a power of two): fixed-depth, branch-free (no divergence
+// between lanes whose searches would take different numbers of steps); pfx[0] = 0 <= g
+template <int N>
+__device__ __forceinline__ int find_record_fixed(const uint32_t* pfx, int nb, uint32_t g) {
+  int k = 0;
+#pragma unroll
+  for (int s = N / 2; s >= 1; s >>= 1) {
+    const int c = k + s;
+    if (c < nb && pfx[c] <= g) k = c;
+  }
+  return k;
+}
+
 template <int W>
 __device__ __forceinline__ void bump(uint32_t* cnt, uint32_t rel, uint32_t par) {
   if (W == 8) {
@@ -298,7 +311,7 @@ __device__ __forceinline__ void walk_pairs(const Params& P, const uint32_t* s_lo
   const uint32_t npairs = (ngroups + 1u) >> 1;
   for (uint32_t gp = threadIdx.x; gp < npairs; gp += T) {
     const uint32_t g = gp << 1;
-    const int k = find_record(s_pfx, nb, g);
+    const int k = find_record_fixed<T>(s_pfx, nb, g);
     const uint32_t lx0 = s_lo[k], hi0 = s_hi[k];
     const uint32_t lo0 = lx0 & 0x7fffffffu, sg0 = lx0 & 0x80000000u;
     const uint32_t grp0 = (lo0 >> 2) + (g - s_pfx[k]);
@@ -407,8 +420,9 @@ struct OpBits {
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
     const uint32_t i = w & 15u;                     // bit i: seen, bit 16 + i: parity
     const uint32_t v = w ^ sg;
-    const uint32_t old = s_atom_or(rb + ((w >> 2) & 0x0ffffffcu), (((v >> 15) & 0x10000u) | 1u) << i);
-    if ((old >> i) & 1u) {
+    const uint32_t one = 1u << i;
+    const uint32_t old = s_atom_or(rb + ((w >> 2) & 0x0ffffffcu), one | ((v >> 31) << (16u + i)));
+    if (old & one) {
       const uint32_t cneg = (v >> 31) & (old >> (16u + i));
       const uint32_t idx = s_atom_add(count, 1u);
       if (idx < Q) s_st(queue + (idx << 2), (w & 0x7fffffffu) | (cneg << 31));
@@ -948,6 +962,10 @@ int configure(Graph& g, Launch& L) {
     case 1024:
       return configure_t<1024, 1>(g, L);
     default:
+      // 128-thread CTAs: 8 per SM (default) or, for experiments (env BBC_MINB), 10 / 12
+      // with fewer registers and smaller tiles
+      if (g.minb == 12) return configure_t<128, 12>(g, L);
+      if (g.minb == 10) return configure_t<128, 10>(g, L);
       return configure_t<128, 8>(g, L);
   }
 }
@@ -957,11 +975,13 @@ int configure_cold(Graph& g, Launch& L) { return configure_t<256, 2>(g, L); }
 
 }  // namespace
 
-// Table granularity: the W16 span of the 128 x 8 configuration (hub band of phase 1).
+// Table granularity: the W16 span of the 128-thread configuration in use (hub band).
 int count_span16(Graph& g) {
   Launch L;
   BBC_CK(cudaSetDevice(g.device));
-  if (configure_t<128, 8>(g, L)) return -1;
+  Graph h = g;
+  h.threads = 128;
+  if (configure(h, L)) return -1;
   return L.cap_words - 8;
 }
 
@@ -1010,7 +1030,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
 
   // tuning knobs (defaults measured on config 2; env overrides for experiments)
   struct {
-    uint32_t rep_slots = 256, bits_thr = 4096, sweep_min = 2, bm_cols0 = 4;
+    uint32_t rep_slots = 256, bits_thr = 4096, sweep_min = 2, bm_cols0 = 8;
   } tune;
   if (const char* e = std::getenv("BBC_BM_COLS0")) tune.bm_cols0 = (uint32_t)std::atoi(e);
   if (const char* e = std::getenv("BBC_REP_SLOTS")) tune.rep_slots = (uint32_t)std::atoi(e);
