@@ -108,6 +108,22 @@ int bbc_graph_create_device(int device, int64_t n_u, int64_t n_v, int64_t m, con
  * partitions sum (mod 2^128) to the graph's counts. */
 int bbc_count(bbc_graph* g, const bbc_opts* opts, uint64_t out[2], bbc_stats* stats);
 
+/* six-way butterfly classification, replacing
+ * oracle.classify_butterflies (pkg/src/bbcount/oracle.py:172-197).  Anchors U-pairs over
+ * V-centres, so the graph must have been built with side_rule BBC_SIDE_U (else
+ * BBC_ERR_ARG).  out[2i], out[2i+1] = low / high 64 bits of class i in
+ * ButterflyClassCounts.as_dict() order (oracle.py:56-64): coherent_pp_pp, coherent_pp_mm,
+ * coherent_mm_mm, incoherent_pm_pm, mixed_pp_pm, mixed_pm_mm.  opts: algo, blocks,
+ * part_index / part_count as for bbc_count (partial results sum). */
+int bbc_classify(bbc_graph* g, const bbc_opts* opts, uint64_t out[12], bbc_stats* stats);
+
+/* balanced (2,k)-bicliques, k >= 2, replacing
+ * count_balanced_2k_serial (pkg/src/bbcount/buckets.py:64-154): the size-2 side is the
+ * graph's anchor side (build with BBC_SIDE_U / BBC_SIDE_V to choose it).
+ * out[0], out[1] = low / high 64 bits; BBC_ERR_ARG for k < 2 (InvalidKError);
+ * BBC_ERR_OVERFLOW above 2^64-1 (CountOverflowError). */
+int bbc_count_2k(bbc_graph* g, int32_t k, const bbc_opts* opts, uint64_t out[2], bbc_stats* stats);
+
 /* Per-CTA admitted wedges of the last bbc_count (ScheduleReport.per_block_work). */
 int bbc_block_work(bbc_graph* g, uint64_t* out, int32_t n);
 

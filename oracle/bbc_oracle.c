@@ -22,6 +22,13 @@
  *       pinned against the reference by tests/golden.
  *   - totals are exact 128-bit; > 2^64-1 is the reference's
  *       CountOverflowError (buckets.py:195-196).
+ * Two SURVEY.md 8(f) extensions of the same wedge loop (mode argument):
+ *   - balanced (2,k)-bicliques, k >= 2: closing sum C(b1,k) + C(b2,k) over the
+ *       touched endpoints (buckets.py:64-154, math.comb at :146), anchor side fixed
+ *       by the caller; a total > 2^64-1 is CountOverflowError.
+ *   - six-way classification (oracle.py:172-197): U anchors, V centres; per (u, w)
+ *       the wedge counts n_pp, n_mm, n_pm give C(pp,2), pp*mm, C(mm,2), C(pm,2),
+ *       pp*pm, mm*pm (ButterflyClassCounts.as_dict order).
  * Multithreading mirrors count_balanced_parallel (buckets.py:205-246): anchor
  * ranges pulled dynamically by workers, exact integer sum.
  *
@@ -168,11 +175,25 @@ typedef struct {
   int64_t next;         /* shared chunk cursor */
   pthread_mutex_t lock;
   int64_t chunk;
-  u128 bal, unb;
-  uint64_t admitted, scanned;
+  int mode; /* 0: balanced / unbalanced, 1: (2,k), 2: classification */
+  int k;
 } job;
 
-typedef struct { job* j; u128 bal, unb; uint64_t admitted, scanned; int err; } worker_arg;
+typedef struct { job* j; u128 bal, unb; u128 cls[6]; uint64_t admitted, scanned; int err, ovf; } worker_arg;
+
+/* C(b, k) exactly; sets *ovf (and returns 2^64) once it exceeds 2^64 - 1 */
+static u128 binom_sat(u128 b, int k, int* ovf) {
+  if ((u128)k > b) return 0;
+  u128 kk = (u128)k;
+  if (kk > b - kk) kk = b - kk;
+  u128 r = 1;
+  const u128 lim = (u128)1 << 64;
+  for (u128 i = 1; i <= kk; ++i) {
+    r = r * (b - kk + i) / i;
+    if (r >= lim) { *ovf = 1; return lim; }
+  }
+  return r;
+}
 
 /* buckets.py:166-197 (+ unbalanced = sum b1*b2) over anchors [lo, hi) step stride */
 static void* worker(void* p) {
@@ -187,11 +208,15 @@ static void* worker(void* p) {
   int64_t n = j->n;
   int64_t* b1 = (int64_t*)calloc((size_t)n + 1, 8);
   int64_t* b2 = (int64_t*)calloc((size_t)n + 1, 8);
+  int64_t* b3 = j->mode == 2 ? (int64_t*)calloc((size_t)n + 1, 8) : NULL;
   int64_t* stamp = (int64_t*)malloc(((size_t)n + 1) * 8);
   int64_t* touched = (int64_t*)malloc(((size_t)n + 1) * 8);
-  if (!b1 || !b2 || !stamp || !touched) { wa->err = E_NOMEM; free(b1); free(b2); free(stamp); free(touched); return NULL; }
+  if (!b1 || !b2 || !stamp || !touched || (j->mode == 2 && !b3)) {
+    wa->err = E_NOMEM; free(b1); free(b2); free(b3); free(stamp); free(touched); return NULL;
+  }
   for (int64_t i = 0; i < n; ++i) stamp[i] = -1;
-  u128 bal = 0, unb = 0;
+  u128 bal = 0, unb = 0, cls[6] = {0, 0, 0, 0, 0, 0};
+  int ovf = 0;
   uint64_t admitted = 0, scanned = 0;
   for (;;) {
     pthread_mutex_lock(&j->lock);
@@ -212,35 +237,47 @@ static void* worker(void* p) {
           int32_t w = adj_o[f];
           if (prank[w] < pu) {
             ++admitted;
-            if (stamp[w] != a) { stamp[w] = a; b1[w] = 0; b2[w] = 0; touched[nt++] = w; }
-            if (sgn_o[f] == suv) b1[w]++; else b2[w]++;
+            if (stamp[w] != a) { stamp[w] = a; b1[w] = 0; b2[w] = 0; if (b3) b3[w] = 0; touched[nt++] = w; }
+            if (j->mode == 2) {
+              /* wedge through centre c: pp (both +), mm (both -), pm (signs differ) */
+              if (sgn_o[f] != suv) b3[w]++; else if (suv > 0) b1[w]++; else b2[w]++;
+            } else if (sgn_o[f] == suv) b1[w]++; else b2[w]++;
           }
         }
       }
       for (int64_t t = 0; t < nt; ++t) {
         u128 c1 = (u128)b1[touched[t]], c2 = (u128)b2[touched[t]];
-        bal += c1 * (c1 - (c1 > 0)) / 2 + c2 * (c2 - (c2 > 0)) / 2;
-        unb += c1 * c2;
+        if (j->mode == 0) {
+          bal += c1 * (c1 - (c1 > 0)) / 2 + c2 * (c2 - (c2 > 0)) / 2;
+          unb += c1 * c2;
+        } else if (j->mode == 1) {
+          bal += binom_sat(c1, j->k, &ovf) + binom_sat(c2, j->k, &ovf);
+          if (bal >= ((u128)1 << 64)) ovf = 1;
+        } else {
+          u128 c3 = (u128)b3[touched[t]];
+          cls[0] += c1 * (c1 - (c1 > 0)) / 2;  /* coherent_pp_pp */
+          cls[1] += c1 * c2;                   /* coherent_pp_mm */
+          cls[2] += c2 * (c2 - (c2 > 0)) / 2;  /* coherent_mm_mm */
+          cls[3] += c3 * (c3 - (c3 > 0)) / 2;  /* incoherent_pm_pm */
+          cls[4] += c1 * c3;                   /* mixed_pp_pm */
+          cls[5] += c2 * c3;                   /* mixed_pm_mm */
+        }
       }
     }
   }
-  free(b1); free(b2); free(stamp); free(touched);
-  wa->bal = bal; wa->unb = unb; wa->admitted = admitted; wa->scanned = scanned;
+  free(b1); free(b2); free(b3); free(stamp); free(touched);
+  wa->bal = bal; wa->unb = unb; wa->admitted = admitted; wa->scanned = scanned; wa->ovf = ovf;
+  for (int i = 0; i < 6; ++i) wa->cls[i] = cls[i];
   return NULL;
 }
 
-/*
- * Count balanced / unbalanced butterflies.  side: 0 = U anchors, 1 = V,
- * -1 = reference min_side (graph.py:174-176).  stride > 1 processes the
- * deterministic anchor sample {a : a % stride == 0} (CPU-baseline sampling).
- * out: [bal_lo, bal_hi, unb_lo, unb_hi, admitted, scanned, side_used].
- */
-int bbc_oracle_count(const og_graph* g, int side, int threads, int64_t stride, uint64_t* out) {
+/* the wedge loop over all anchors of `side` in the given mode (see the header) */
+static int run(const og_graph* g, int side, int threads, int64_t stride, int mode, int k, uint64_t* out) {
   if (side < 0) side = g->n_u <= g->n_v ? 0 : 1;
   if (threads < 1 || stride < 1) return E_ARG;
   job j;
   memset(&j, 0, sizeof(j));
-  j.g = g; j.side = side; j.n = side == 0 ? g->n_u : g->n_v; j.stride = stride;
+  j.g = g; j.side = side; j.n = side == 0 ? g->n_u : g->n_v; j.stride = stride; j.mode = mode; j.k = k;
   pthread_mutex_init(&j.lock, NULL);
   int64_t target = (int64_t)threads * 64;
   j.chunk = j.n / (target > 0 ? target : 1);
@@ -251,20 +288,48 @@ int bbc_oracle_count(const og_graph* g, int side, int threads, int64_t stride, u
   for (int t = 1; t < threads; ++t) pthread_create(&th[t], NULL, worker, &wa[t]);
   worker(&wa[0]);
   for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
-  u128 bal = 0, unb = 0;
+  u128 bal = 0, unb = 0, cls[6] = {0, 0, 0, 0, 0, 0};
   uint64_t adm = 0, scn = 0;
-  int err = OK;
+  int err = OK, ovf = 0;
   for (int t = 0; t < threads; ++t) {
     bal += wa[t].bal; unb += wa[t].unb; adm += wa[t].admitted; scn += wa[t].scanned;
+    for (int i = 0; i < 6; ++i) cls[i] += wa[t].cls[i];
     if (wa[t].err) err = wa[t].err;
+    ovf |= wa[t].ovf;
   }
   free(th); free(wa);
   pthread_mutex_destroy(&j.lock);
   out[0] = (uint64_t)bal; out[1] = (uint64_t)(bal >> 64);
   out[2] = (uint64_t)unb; out[3] = (uint64_t)(unb >> 64);
   out[4] = adm; out[5] = scn; out[6] = (uint64_t)side;
+  if (mode == 2)
+    for (int i = 0; i < 6; ++i) { out[8 + 2 * i] = (uint64_t)cls[i]; out[9 + 2 * i] = (uint64_t)(cls[i] >> 64); }
   if (err) return err;
+  if (mode == 1) return (ovf || out[1]) ? E_OVERFLOW : OK;
   return (out[1] || out[3]) ? E_OVERFLOW : OK;
+}
+
+/*
+ * Count balanced / unbalanced butterflies.  side: 0 = U anchors, 1 = V,
+ * -1 = reference min_side (graph.py:174-176).  stride > 1 processes the
+ * deterministic anchor sample {a : a % stride == 0} (CPU-baseline sampling).
+ * out: [bal_lo, bal_hi, unb_lo, unb_hi, admitted, scanned, side_used].
+ */
+int bbc_oracle_count(const og_graph* g, int side, int threads, int64_t stride, uint64_t* out) {
+  return run(g, side, threads, stride, 0, 2, out);
+}
+
+/* Balanced (2,k)-bicliques with the size-2 side `side` (0 = U, 1 = V): out[0..1] = the
+ * total (lo, hi); E_OVERFLOW once it exceeds 2^64 - 1 (out then saturated / partial). */
+int bbc_oracle_count_2k(const og_graph* g, int side, int k, int threads, uint64_t* out) {
+  if (k < 2 || side < 0 || side > 1) return E_ARG;
+  return run(g, side, threads, 1, 1, k, out);
+}
+
+/* Six-way classification (U anchors): out[8 + 2i], out[9 + 2i] = lo, hi of class i in
+ * ButterflyClassCounts.as_dict order; out must hold 20 words. */
+int bbc_oracle_classify(const og_graph* g, int threads, uint64_t* out) {
+  return run(g, 0, threads, 1, 2, 2, out);
 }
 
 int64_t bbc_oracle_graph_info(const og_graph* g, int what) {

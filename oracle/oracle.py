@@ -49,6 +49,10 @@ def _load():
         L.bbc_oracle_count.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int64, P]
         L.bbc_oracle_graph_free.argtypes = [P]
         L.bbc_oracle_graph_free.restype = None
+        L.bbc_oracle_count_2k.restype = ctypes.c_int
+        L.bbc_oracle_count_2k.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P]
+        L.bbc_oracle_classify.restype = ctypes.c_int
+        L.bbc_oracle_classify.argtypes = [P, ctypes.c_int, P]
         L.bbc_oracle_admitted_total.restype = ctypes.c_uint64
         L.bbc_oracle_admitted_total.argtypes = [P, ctypes.c_int]
         _lib = L
@@ -95,6 +99,26 @@ class OracleGraph:
             raise OracleError(rc, 0)
         return OracleResult(balanced=int(out[0]) | (int(out[1]) << 64), unbalanced=int(out[2]) | (int(out[3]) << 64),
                             admitted=int(out[4]), scanned=int(out[5]), side=int(out[6]))
+
+    def count_2k(self, k: int, side: int, threads: int | None = None) -> tuple[int, bool]:
+        """Balanced (2,k)-bicliques with the size-2 side ``side`` (buckets.py:64-154):
+        (total, overflowed past 2^64 - 1)."""
+        out = (ctypes.c_uint64 * 8)()
+        rc = _load().bbc_oracle_count_2k(self._h, side, k, threads or len(os.sched_getaffinity(0)), out)
+        if rc not in (0, E_OVERFLOW):
+            raise OracleError(rc, 0)
+        return int(out[0]) | (int(out[1]) << 64), rc == E_OVERFLOW
+
+    CLASS_NAMES = ("coherent_pp_pp", "coherent_pp_mm", "coherent_mm_mm", "incoherent_pm_pm", "mixed_pp_pm",
+                   "mixed_pm_mm")
+
+    def classify(self, threads: int | None = None) -> dict[str, int]:
+        """Six-way butterfly classification (oracle.py:172-197), as_dict() keys."""
+        out = (ctypes.c_uint64 * 20)()
+        rc = _load().bbc_oracle_classify(self._h, threads or len(os.sched_getaffinity(0)), out)
+        if rc not in (0, E_OVERFLOW):
+            raise OracleError(rc, 0)
+        return {n: int(out[8 + 2 * i]) | (int(out[9 + 2 * i]) << 64) for i, n in enumerate(self.CLASS_NAMES)}
 
     def admitted_total(self, side: int) -> int:
         return int(_load().bbc_oracle_admitted_total(self._h, side))

@@ -31,7 +31,7 @@ FLAG_ROUNDS = 4096  # record per-kind round counters (round_counters())
 
 EXPORTED_SYMBOLS = (
     "bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work", "bbc_task_order",
-    "bbc_round_counters", "bbc_graph_info", "bbc_graph_stream", "bbc_graph_destroy", "bbc_device_count", "bbc_last_error",
+    "bbc_round_counters", "bbc_classify", "bbc_count_2k", "bbc_graph_info", "bbc_graph_stream", "bbc_graph_destroy", "bbc_device_count", "bbc_last_error",
     "bbc_last_error_info",
 )
 
@@ -70,6 +70,8 @@ def load() -> ctypes.CDLL:
         L.bbc_block_work.argtypes = [P, U64P, I32]
         L.bbc_task_order.argtypes = [P, I32, ctypes.POINTER(ctypes.c_int32), P, I64]
         L.bbc_round_counters.argtypes = [P, U64P]
+        L.bbc_classify.argtypes = [P, ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
+        L.bbc_count_2k.argtypes = [P, I32, ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
         L.bbc_graph_info.argtypes = [P, ctypes.POINTER(ctypes.c_int64), I32]
         L.bbc_graph_stream.argtypes = [P]
         L.bbc_graph_stream.restype = P
@@ -79,7 +81,8 @@ def load() -> ctypes.CDLL:
         L.bbc_last_error.restype = ctypes.c_char_p
         L.bbc_last_error_info.restype = ctypes.c_int64
         for name in ("bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work",
-                     "bbc_task_order", "bbc_round_counters", "bbc_graph_info", "bbc_device_count"):
+                     "bbc_task_order", "bbc_round_counters", "bbc_classify", "bbc_count_2k", "bbc_graph_info",
+                     "bbc_device_count"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
         return L
@@ -174,6 +177,37 @@ class DeviceGraph:
                            anchor_side=int(st.anchor_side), blocks=int(st.blocks), threads=int(st.threads),
                            tile_span=int(st.tile_span), tasks=int(st.tasks), preprocess_ms=float(st.preprocess_ms),
                            count_ms=float(st.count_ms))
+
+    CLASS_NAMES = ("coherent_pp_pp", "coherent_pp_mm", "coherent_mm_mm", "incoherent_pm_pm", "mixed_pp_pm",
+                   "mixed_pm_mm")
+
+    def classify(self, algo: int = ALGO_GBBCPP, blocks: int = 0, part_index: int = 0,
+                 part_count: int = 1) -> tuple[dict[str, int], float]:
+        """Six-way classification (needs a U-anchored handle): (as_dict() counts, device ms)."""
+        if self._h is None:
+            raise DeviceError("graph handle already closed")
+        o = Opts(algo=algo, blocks=blocks, part_index=part_index, part_count=part_count)
+        out = (ctypes.c_uint64 * 12)()
+        st = Stats()
+        rc = load().bbc_classify(self._h, ctypes.byref(o), out, ctypes.byref(st))
+        if rc:
+            _raise(rc)
+        return ({n: int(out[2 * i]) | (int(out[2 * i + 1]) << 64) for i, n in enumerate(self.CLASS_NAMES)},
+                float(st.count_ms))
+
+    def count_2k(self, k: int, algo: int = ALGO_GBBCPP, blocks: int = 0, part_index: int = 0,
+                 part_count: int = 1) -> tuple[int, bool, float]:
+        """Balanced (2,k)-bicliques with the size-2 side = this handle's anchor side:
+        (count, overflowed past 2^64 - 1, device ms)."""
+        if self._h is None:
+            raise DeviceError("graph handle already closed")
+        o = Opts(algo=algo, blocks=blocks, part_index=part_index, part_count=part_count)
+        out = (ctypes.c_uint64 * 2)()
+        st = Stats()
+        rc = load().bbc_count_2k(self._h, k, ctypes.byref(o), out, ctypes.byref(st))
+        if rc and rc != 3:
+            _raise(rc)
+        return int(out[0]) | (int(out[1]) << 64), rc == 3, float(st.count_ms)
 
     def block_work(self, n: int) -> list[int]:
         buf = (ctypes.c_uint64 * max(n, 1))()

@@ -8,6 +8,8 @@
 namespace bbc {
 
 int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st);
+int classify_graph(Graph& g, const bbc_opts* o, uint64_t out[12], bbc_stats* st);
+int count_2k_graph(Graph& g, int32_t k, const bbc_opts* o, uint64_t out[2], bbc_stats* st);
 
 namespace {
 thread_local std::string t_err;
@@ -36,6 +38,22 @@ int bbc_count(bbc_graph* h, const bbc_opts* opts, uint64_t out[2], bbc_stats* st
   }
   if (stats) std::memset(stats, 0, sizeof(*stats));
   return bbc::count_graph(h->g, opts, out, stats);
+}
+
+int bbc_classify(bbc_graph* h, const bbc_opts* opts, uint64_t out[12], bbc_stats* stats) {
+  if (!h || !out) {
+    bbc::set_error("graph handle and out must not be null");
+    return BBC_ERR_ARG;
+  }
+  return bbc::classify_graph(h->g, opts, out, stats);
+}
+
+int bbc_count_2k(bbc_graph* h, int32_t k, const bbc_opts* opts, uint64_t out[2], bbc_stats* stats) {
+  if (!h || !out) {
+    bbc::set_error("graph handle and out must not be null");
+    return BBC_ERR_ARG;
+  }
+  return bbc::count_2k_graph(h->g, k, opts, out, stats);
 }
 
 int bbc_block_work(bbc_graph* h, uint64_t* out, int32_t n) {

@@ -31,12 +31,12 @@
 #include <string>
 
 #include "bbc_internal.cuh"
+#include "bbc_walk.cuh"
 
 namespace bbc {
 
 namespace {
 
-constexpr uint32_t kFull = 0xffffffffu;
 
 enum Mode { kDense = 0, kSparse = 1, kZero = 2 };
 
@@ -77,92 +77,6 @@ struct Params {
   unsigned int* queue;
   unsigned long long* block_work;
 };
-
-__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-// first position in [lo, hi) whose rank is >= x (lists are rank-sorted)
-__device__ __forceinline__ uint32_t lower_bound_rank(const uint32_t* __restrict__ adj, uint32_t lo, uint32_t hi,
-                                                     long long x) {
-  if (x <= 0) return lo;
-  while (lo < hi) {
-    uint32_t mid = (lo + hi) >> 1;
-    if ((long long)(__ldg(adj + mid) & 0x7fffffffu) < x)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
-}
-
-// Block-wide exclusive scan of one u32 per thread fused with a u64 sum, with ONE barrier:
-// each warp publishes its totals, then every warp scans the (<= 32) warp totals itself.
-// The totals are double-buffered by `buf` (callers alternate it), since consecutive scans
-// may have no other barrier between them and a warp can be one scan ahead.
-template <int T>
-__device__ __forceinline__ uint32_t scan_sum(uint32_t v, unsigned long long w, uint32_t& total,
-                                             unsigned long long& wtotal, uint32_t* s_v, unsigned long long* s_w,
-                                             uint32_t buf) {
-  constexpr int kWarps = T / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(kFull, x, o);
-    if (lane >= o) x += y;
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(kFull, w, o);
-  uint32_t* sv = s_v + (buf & 1u) * 32u;
-  unsigned long long* sw = s_w + (buf & 1u) * 32u;
-  if (lane == 31) sv[warp] = x;
-  if (lane == 0) sw[warp] = w;
-  __syncthreads();
-  uint32_t a = lane < kWarps ? sv[lane] : 0u;
-  unsigned long long bsum = lane < kWarps ? sw[lane] : 0ull;
-#pragma unroll
-  for (int o = 1; o < kWarps; o <<= 1) {
-    uint32_t y = __shfl_up_sync(kFull, a, o);
-    if (lane >= o) a += y;
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) bsum += __shfl_xor_sync(kFull, bsum, o);
-  total = __shfl_sync(kFull, a, kWarps - 1);
-  wtotal = bsum;
-  const uint32_t before = __shfl_sync(kFull, a, (warp + 31) & 31);  // inclusive prefix of warp - 1
-  return x - v + (warp > 0 ? before : 0u);
-}
-
-// largest k in [0, nb) with pfx[k] <= g
-__device__ __forceinline__ int find_record(const uint32_t* pfx, int nb, uint32_t g) {
-  int lo = 0, hi = nb;
-  while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (pfx[mid] <= g)
-      lo = mid;
-    else
-      hi = mid;
-  }
-  return lo;
-}
-
-// the same for nb <= N (a power of two): fixed-depth, branch-free (no divergence
-// between lanes whose searches would take different numbers of steps); pfx[0] = 0 <= g
-template <int N>
-__device__ __forceinline__ int find_record_fixed(const uint32_t* pfx, int nb, uint32_t g) {
-  int k = 0;
-#pragma unroll
-  for (int s = N / 2; s >= 1; s >>= 1) {
-    const int c = k + s;
-    if (c < nb && pfx[c] <= g) k = c;
-  }
-  return k;
-}
 
 template <int W>
 __device__ __forceinline__ void bump(uint32_t* cnt, uint32_t rel, uint32_t par) {
@@ -265,76 +179,6 @@ __device__ __forceinline__ void hash_bump_close(uint32_t* tab, uint32_t K, uint3
   const uint32_t old = atomicAdd(&tab[2u * h + 1u], 1u << sh);
   tb += (old >> sh) & 0xffffu;
   tu += (old >> (sh ^ 16u)) & 0xffffu;
-}
-
-// ---- shared-memory primitives on 32-bit shared addresses ------------------------------
-// (generic pointers make the compiler re-derive the shared window base per access)
-// (the move is opaque to the compiler, so a base address stays in one register instead of
-// being re-derived from the CTA's shared window before every atomic)
-__device__ __forceinline__ uint32_t sptr(const void* p) {
-  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
-  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(a));
-  return r;
-}
-__device__ __forceinline__ uint32_t s_atom_add(uint32_t a, uint32_t v) {
-  uint32_t r;
-  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
-  return r;
-}
-__device__ __forceinline__ uint32_t s_atom_or(uint32_t a, uint32_t v) {
-  uint32_t r;
-  asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
-  return r;
-}
-__device__ __forceinline__ void s_red_add(uint32_t a, uint32_t v) {
-  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-__device__ __forceinline__ void s_st(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-
-// valid slots (bits 0..3) of the int4 group starting at word position p0 for [lo, hi)
-__device__ __forceinline__ uint32_t slot_mask(uint32_t p0, uint32_t lo, uint32_t hi) {
-  const int a = max((int)(lo - p0), 0);
-  const int b = min((int)(hi - p0), 4);
-  return b <= a ? 0u : (((1u << b) - 1u) & (0xfu << a));
-}
-
-// Walk the int4 groups of the round's sub-slices, a PAIR of consecutive groups per thread
-// per iteration (one record search per pair; the second group usually lies in the same
-// record).  Both loads are issued before either group is processed.  op.wedge(word,
-// sign, slot) runs for every valid wedge; op.flush() after each pair.
-template <int T, class Op>
-__device__ __forceinline__ void walk_pairs(const Params& P, const uint32_t* s_lo, const uint32_t* s_hi,
-                                           const uint32_t* s_pfx, int nb, uint32_t ngroups, Op& op) {
-  const uint4* adj4 = reinterpret_cast<const uint4*>(P.adj);
-  const uint32_t npairs = (ngroups + 1u) >> 1;
-  for (uint32_t gp = threadIdx.x; gp < npairs; gp += T) {
-    const uint32_t g = gp << 1;
-    const int k = find_record_fixed<T>(s_pfx, nb, g);
-    const uint32_t lx0 = s_lo[k], hi0 = s_hi[k];
-    const uint32_t lo0 = lx0 & 0x7fffffffu, sg0 = lx0 & 0x80000000u;
-    const uint32_t grp0 = (lo0 >> 2) + (g - s_pfx[k]);
-    const bool has1 = g + 1u < ngroups;
-    uint32_t lo1 = lo0, hi1 = hi0, sg1 = sg0, grp1 = grp0 + 1u;
-    if (has1 && k + 1 < nb && s_pfx[k + 1] <= g + 1u) {
-      int k1 = k + 1;
-      while (k1 + 1 < nb && s_pfx[k1 + 1] <= g + 1u) ++k1;
-      const uint32_t lx1 = s_lo[k1];
-      lo1 = lx1 & 0x7fffffffu;
-      sg1 = lx1 & 0x80000000u;
-      hi1 = s_hi[k1];
-      grp1 = (lo1 >> 2) + (g + 1u - s_pfx[k1]);
-    }
-    const uint4 q0 = ld_stream(adj4 + grp0);
-    const uint4 q1 = has1 ? ld_stream(adj4 + grp1) : make_uint4(0u, 0u, 0u, 0u);
-    const uint32_t m = slot_mask(grp0 << 2, lo0, hi0) | (has1 ? slot_mask(grp1 << 2, lo1, hi1) << 4 : 0u);
-    const uint32_t wv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (m & (1u << j)) op.wedge(wv[j], j < 4 ? sg0 : sg1, j);
-    op.flush();
-  }
 }
 
 // The tile / bitmap ops address their words from a REBASED shared address: rb = base -
@@ -657,7 +501,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       OpTileClose<W, true> op{base, &tb, &tu};
 #pragma unroll
       for (int j = 0; j < 8; ++j) op.touched[j] = 0xffffffffu;
-      walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ngroups, op);
+      walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < 8; ++j)
@@ -666,14 +510,14 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       // medium rounds: inline closing, then the tile is cleared with vector stores (a
       // closing sweep costs ~9 instructions per counter word, inline closing ~4 per wedge)
       OpTileClose<W, false> op{base, &tb, &tu};
-      walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ngroups, op);
+      walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
       uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
       for (uint32_t i = threadIdx.x; i < (band_words + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
     } else {
       // dense rounds: no-return increments and the shared-memory closing sweep
       OpTileDense<W> op{base};
-      walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ngroups, op);
+      walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
       sweep<T, W>(S.cnt, band_words, tb, tu);
     }
@@ -684,7 +528,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     if ((P.debug & 4096) && threadIdx.x == 0) atomicAdd(P.acc + 7, 1ull);
     const uint32_t K = min(P.hslots, max(64u, (uint32_t)(2ull * bw + 31ull) & ~31u));
     OpHash op{S.cnt, K, &tb, &tu};
-    walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ngroups, op);
+    walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
     __syncthreads();
     uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
     for (uint32_t i = threadIdx.x; i < (2u * K + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -751,7 +595,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       uint32_t* keys = queue + Q;
       uint32_t* vals = keys + K;
       OpBits op{sptr(bm) - ((lo_rank >> 4) << 2), sptr(queue), sptr(cnt), Q};
-      walk_pairs<T>(P, S.lo, S.hi, S.pfx, nb, ng, op);
+      walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ng, op);
       __syncthreads();
       const uint32_t nq = *cnt;
       const bool ovf = nq > Q;

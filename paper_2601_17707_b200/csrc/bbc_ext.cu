@@ -1,0 +1,451 @@
+// SURVEY.md 8(f) kernels on the same device CSR as the count kernel:
+//
+//   * six-way butterfly classification -- reference oracle.classify_butterflies
+//     (pkg/src/bbcount/oracle.py:172-197, ButterflyClassCounts :31-64).  Anchors are U
+//     vertices, centres V (the classes are not side-symmetric, oracle.py:176-178), so the
+//     graph must be built with BBC_SIDE_U.  For every anchor pair (u, w) the wedges
+//     through the common centres c split into pp (both edges +), mm (both -) and pm
+//     (signs differ); the classes are C(pp,2), pp*mm, C(mm,2), C(pm,2), pp*pm, mm*pm.
+//   * balanced (2,k)-bicliques, k >= 2 -- reference count_balanced_2k_serial
+//     (pkg/src/bbcount/buckets.py:64-154): per pair C(b1,k) + C(b2,k) with b1 / b2 the
+//     symmetric / asymmetric wedge counts (math.comb at :146), the size-2 side = the
+//     graph's anchor side; a total above 2^64-1 is CountOverflowError.
+//
+// Structure (one CTA per anchor, persistent CTAs over the G-BBC++ queue or static
+// round-robin): the anchor's end-vertex ranks are cut into bands of S ranks from the top;
+// per band and per batch of <= T records, each record's admitted sub-slice is found by
+// binary search (the next band's upper bound is carried), a block scan lays the int4
+// groups out and the pair walker (bbc_walk.cuh) increments a shared-memory counter per end
+// vertex.  Closing is inline from the atomic's return value wherever one atomic returns
+// every count of the end vertex:
+//   (2,k) W16: u16 b1 | u16 b2 per end vertex (deg u <= 65535), W32: two words; adding a
+//        wedge to a bucket holding c adds C(c, k-1) = C(c+1, k) - C(c, k);
+//   classify C10: pp | mm << 10 | pm << 20 (deg u <= 1023): adding a pp wedge to (a, b, d)
+//        adds a to C(pp,2), b to pp*mm and d to pp*pm (likewise for mm and pm);
+//   classify C32 (deg u > 1023): three words, no-return increments and a closing sweep.
+// Totals are exact 128-bit per thread, reduced with one pair of atomics per warp.
+#include <cstring>
+
+#include "bbc_internal.cuh"
+#include "bbc_walk.cuh"
+
+namespace bbc {
+
+namespace {
+
+enum ExtMode { kClassify = 0, kBicliques = 1 };
+
+struct ExtParams {
+  const uint32_t* __restrict__ adj;
+  const uint2* __restrict__ rec;
+  const uint32_t* __restrict__ coff;
+  const uint32_t* __restrict__ aoff;
+  const unsigned long long* __restrict__ awork;
+  const uint32_t* __restrict__ order;
+  uint32_t n, ntasks, part_index, part_count;
+  uint32_t cap_words;
+  uint32_t k1;  // (2,k): k - 1
+  int dynamic;
+  unsigned long long* acc;  // 6 x (lo, hi) + [12] overflow flag
+  unsigned int* queue;
+  unsigned long long* block_work;
+};
+
+__device__ __forceinline__ void add128(unsigned long long& lo, unsigned long long& hi, unsigned long long x) {
+  lo += x;
+  hi += (lo < x) ? 1ull : 0ull;
+}
+
+// C(c, j) for c >= j >= 1, exact below 2^64; ~0 (the overflow marker) above
+__device__ __forceinline__ unsigned long long binom_dev(unsigned long long c, uint32_t j) {
+  unsigned __int128 r = 1;
+  if ((unsigned long long)j > c - j) j = (uint32_t)(c - j);
+  for (uint32_t i = 1; i <= j; ++i) {
+    r = r * (unsigned __int128)(c - j + i) / i;
+    if (r >> 64) return ~0ull;
+  }
+  return (unsigned long long)r;
+}
+
+// the ops keep their partial sums as members (registers once inlined); the caller adds
+// them to its 128-bit totals after the walk
+
+// (2,k), u16 b1 | u16 b2 per end vertex; rb rebased by lo_rank * 4
+struct OpBiclW16 {
+  uint32_t rb, k1;
+  unsigned long long lo = 0, hi = 0;
+  uint32_t ovf = 0;
+  __device__ __forceinline__ void add(uint32_t c) {
+    const unsigned long long x = k1 == 1u ? (unsigned long long)c : binom_dev(c, k1);
+    if (x == ~0ull) ovf = 1u;
+    lo += x;
+    hi += (lo < x) ? 1ull : 0ull;
+  }
+  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
+    const uint32_t sh = ((w ^ sg) >> 27) & 16u;
+    const uint32_t c = (s_atom_add(rb + (w << 2), 1u << sh) >> sh) & 0xffffu;
+    if (c >= k1) add(c);
+  }
+  __device__ __forceinline__ void flush() {}
+};
+
+// (2,k), two u32 words per end vertex; rb rebased by lo_rank * 8
+struct OpBiclW32 : OpBiclW16 {
+  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
+    const uint32_t c = s_atom_add(rb + (w << 3) + (((w ^ sg) >> 29) & 4u), 1u);
+    if (c >= k1) add(c);
+  }
+};
+
+// wedge class: 0 pp, 1 mm, 2 pm (sg = s(u, c) in bit 31, word bit 31 = s(c, w))
+__device__ __forceinline__ uint32_t wedge_class(uint32_t w, uint32_t sg) {
+  return ((w ^ sg) >> 31) ? 2u : (sg >> 31);
+}
+
+// classification, pp | mm << 10 | pm << 20 per end vertex (deg u <= 1023)
+struct OpClsC10 {
+  uint32_t rb;
+  unsigned long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0;
+  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
+    const uint32_t t = wedge_class(w, sg);
+    const uint32_t old = s_atom_add(rb + (w << 2), 1u << (10u * t));
+    const uint32_t a = old & 1023u, b = (old >> 10) & 1023u, d = old >> 20;
+    if (t == 0u) {  // pp: C(pp,2) += pp, pp*mm += mm, pp*pm += pm
+      c0 += a;
+      c1 += b;
+      c4 += d;
+    } else if (t == 1u) {  // mm
+      c2 += b;
+      c1 += a;
+      c5 += d;
+    } else {  // pm
+      c3 += d;
+      c4 += a;
+      c5 += b;
+    }
+  }
+  __device__ __forceinline__ void flush() {}
+};
+
+// classification, three u32 words per end vertex, closed by the sweep; rb rebased by
+// lo_rank * 12
+struct OpClsC32 {
+  uint32_t rb;
+  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
+    s_red_add(rb + (w & 0x7fffffffu) * 12u + 4u * wedge_class(w, sg), 1u);
+  }
+  __device__ __forceinline__ void flush() {}
+};
+
+struct ExtSmem {
+  uint32_t* cnt;
+  uint32_t *lo, *hi, *pfx;
+  uint32_t* v;
+  unsigned long long* w;
+};
+
+// One anchor: bands from the top, record batches of T, inline closing (or the C32 sweep).
+template <int T, int MODE>
+__device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uint32_t rb, uint32_t re,
+                           unsigned long long (&acc)[12], uint32_t& ovf, unsigned long long& work) {
+  const uint32_t deg = re - rb;
+  const bool wide = MODE == kClassify ? deg > 1023u : deg > 65535u;
+  const uint32_t wpv = wide ? (MODE == kClassify ? 3u : 2u) : 1u;  // words per end vertex
+  const uint32_t span = P.cap_words / wpv;
+  const uint32_t nbands = (P.n - 1u - r) / span + 1u;  // bands 0..nbands-1 hold ranks > r
+  const bool single = deg <= (uint32_t)T;
+  const uint32_t base = sptr(S.cnt);
+  uint32_t scan_buf = 0;
+  uint32_t carry = 0;  // single batch: this record's upper bound for the next band
+  unsigned long long part[6] = {0, 0, 0, 0, 0, 0};
+  for (uint32_t b = 0; b < nbands; ++b) {
+    const long long top = (long long)P.n - (long long)b * span;
+    const long long bot = top - (long long)span;
+    const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
+    const uint32_t band_words = (uint32_t)(top - (long long)lo_rank) * wpv;
+    unsigned long long band_w = 0;
+    for (uint32_t b0 = rb; b0 < re; b0 += T) {
+      const int nb = (int)min((uint32_t)T, re - b0);
+      uint32_t ng = 0;
+      unsigned long long myw = 0;
+      if ((int)threadIdx.x < nb) {
+        const uint2 rr = P.rec[b0 + threadIdx.x];
+        const uint32_t begin = rr.x & 0x7fffffffu;
+        uint32_t hi;
+        if (b == 0)
+          hi = __ldg(P.coff + rr.y + 1);
+        else if (single)
+          hi = carry;
+        else
+          hi = lower_bound_rank(P.adj, begin, __ldg(P.coff + rr.y + 1), top);
+        const uint32_t lo = lower_bound_rank(P.adj, begin, hi, bot);
+        carry = lo;
+        if (hi > lo) {
+          ng = ((hi + 3u) >> 2) - (lo >> 2);
+          myw = hi - lo;
+        }
+        S.lo[threadIdx.x] = lo | (rr.x & 0x80000000u);
+        S.hi[threadIdx.x] = hi;
+      }
+      uint32_t ngroups;
+      unsigned long long bw;
+      const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w, scan_buf++);
+      if ((int)threadIdx.x < nb) S.pfx[threadIdx.x] = ex;
+      __syncthreads();
+      work += myw;
+      band_w += bw;
+      if (ngroups) {
+        if (MODE == kBicliques) {
+          OpBiclW16 x;
+          if (!wide) {
+            OpBiclW16 op;
+            op.rb = base - (lo_rank << 2);
+            op.k1 = P.k1;
+            walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+            x = op;
+          } else {
+            OpBiclW32 op;
+            op.rb = base - (lo_rank << 3);
+            op.k1 = P.k1;
+            walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+            x = op;
+          }
+          add128(acc[0], acc[1], x.lo);
+          acc[1] += x.hi;
+          ovf |= x.ovf;
+        } else if (!wide) {
+          OpClsC10 op;
+          op.rb = base - (lo_rank << 2);
+          walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+          part[0] += op.c0;
+          part[1] += op.c1;
+          part[2] += op.c2;
+          part[3] += op.c3;
+          part[4] += op.c4;
+          part[5] += op.c5;
+        } else {
+          OpClsC32 op{base - lo_rank * 12u};
+          walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+        }
+      }
+      __syncthreads();  // the next batch overwrites the record arrays
+    }
+    if (band_w == 0ull) continue;
+    uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
+    const uint32_t nq = (band_words + 3u) / 4u;
+    if (MODE == kClassify && wide) {
+      // closing sweep over (pp, mm, pm) triples
+      for (uint32_t i = threadIdx.x; i < (band_words / 3u); i += T) {
+        const unsigned long long a = S.cnt[3u * i], bb = S.cnt[3u * i + 1u], d = S.cnt[3u * i + 2u];
+        part[0] += a * (a - (a > 0)) / 2;
+        part[1] += a * bb;
+        part[2] += bb * (bb - (bb > 0)) / 2;
+        part[3] += d * (d - (d > 0)) / 2;
+        part[4] += a * d;
+        part[5] += bb * d;
+      }
+      __syncthreads();
+    }
+    for (uint32_t i = threadIdx.x; i < nq; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+  }
+  if (MODE == kClassify)
+    for (int i = 0; i < 6; ++i) add128(acc[2 * i], acc[2 * i + 1], part[i]);
+}
+
+template <int T, int MINB, int MODE>
+__global__ void __launch_bounds__(T, MINB) k_ext(ExtParams P) {
+  extern __shared__ uint4 smem4[];
+  __shared__ uint32_t s_v[64];
+  __shared__ unsigned long long s_w[64];
+  __shared__ uint32_t s_task;
+  __shared__ uint32_t s_ovf;
+  ExtSmem S;
+  S.cnt = reinterpret_cast<uint32_t*>(smem4);
+  S.lo = S.cnt + P.cap_words;
+  S.hi = S.lo + T;
+  S.pfx = S.hi + T;
+  S.v = s_v;
+  S.w = s_w;
+  for (uint32_t i = threadIdx.x; i < P.cap_words / 4; i += T) smem4[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (threadIdx.x == 0) s_ovf = 0u;
+
+  unsigned long long acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long work = 0;
+  uint32_t ovf = 0;
+  uint32_t next = blockIdx.x;
+  if (threadIdx.x == 0) s_task = P.dynamic ? atomicAdd(P.queue, 1u) : next;
+  __syncthreads();
+  for (;;) {
+    const uint32_t t = s_task;
+    next += gridDim.x;
+    __syncthreads();
+    if (t >= P.ntasks) break;
+    if (threadIdx.x == 0) s_task = P.dynamic ? atomicAdd(P.queue, 1u) : next;
+    const uint32_t gidx = P.part_index + t * P.part_count;
+    const uint32_t r = P.dynamic ? P.order[gidx] : gidx;
+    if (P.awork[r] != 0ull) ext_anchor<T, MODE>(P, S, r, P.aoff[r], P.aoff[r + 1], acc, ovf, work);
+    __syncthreads();
+  }
+  // exact reduction: warp shuffle of the 128-bit values, one pair of atomics per warp
+  const int lane = threadIdx.x & 31;
+  constexpr int kVals = MODE == kClassify ? 6 : 1;
+#pragma unroll
+  for (int i = 0; i < kVals; ++i) {
+    unsigned long long lo = acc[2 * i], hi = acc[2 * i + 1];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long l2 = __shfl_xor_sync(kFull, lo, o), h2 = __shfl_xor_sync(kFull, hi, o);
+      lo += l2;
+      hi += h2 + (lo < l2 ? 1ull : 0ull);
+    }
+    if (lane == 0) {
+      const unsigned long long old = atomicAdd(&P.acc[2 * i], lo);
+      atomicAdd(&P.acc[2 * i + 1], hi + (old + lo < old ? 1ull : 0ull));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) work += __shfl_xor_sync(kFull, work, o);
+  if (ovf) atomicOr(&s_ovf, 1u);
+  if (lane == 0) s_w[threadIdx.x >> 5] = work;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tw = 0;
+    for (int w = 0; w < T / 32; ++w) tw += s_w[w];
+    P.block_work[blockIdx.x] = tw;
+    if (s_ovf) atomicOr(&P.acc[12], 1ull);
+  }
+}
+
+template <int MODE>
+int ext_launch(Graph& g, const bbc_opts& opts, uint32_t k, unsigned long long* h_acc, float* ms, int* blocks_out) {
+  constexpr int T = 128, MINB = 8;
+  cudaFuncAttributes fa;
+  BBC_CK(cudaFuncGetAttributes(&fa, k_ext<T, MINB, MODE>));
+  int per_sm = 0;
+  BBC_CK(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, g.device));
+  const int budget = std::min(g.max_smem, per_sm / MINB - 1024);
+  const int avail = budget - (int)fa.sharedSizeBytes - (3 * T * 4 + 64);
+  const int cap_words = (avail / 48) * 12;  // a multiple of 12 (C32 triples, uint4 clearing)
+  const int smem_bytes = cap_words * 4 + 3 * T * 4 + 16;
+  BBC_CK(cudaFuncSetAttribute(k_ext<T, MINB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  const int blocks = opts.blocks > 0 ? opts.blocks : g.num_sms * MINB;
+  if (blocks > g.block_work_cap) {
+    cudaFree(g.block_work);
+    g.block_work = nullptr;
+    BBC_CK(cudaMalloc(&g.block_work, (size_t)blocks * 8));
+    g.block_work_cap = blocks;
+  }
+  const int part_count = opts.part_count <= 0 ? 1 : opts.part_count;
+  const uint32_t n = (uint32_t)g.n;
+  ExtParams P;
+  P.adj = g.adj;
+  P.rec = g.rec;
+  P.coff = g.coff;
+  P.aoff = g.aoff;
+  P.awork = g.awork;
+  P.order = g.order;
+  P.n = n;
+  P.ntasks = n > (uint32_t)opts.part_index ? (n - (uint32_t)opts.part_index + part_count - 1) / part_count : 0u;
+  P.part_index = (uint32_t)opts.part_index;
+  P.part_count = (uint32_t)part_count;
+  P.cap_words = (uint32_t)cap_words;
+  P.k1 = k - 1u;
+  P.dynamic = opts.algo == BBC_ALGO_GBBCPP;
+  P.acc = g.acc;
+  P.queue = g.queue;
+  P.block_work = g.block_work;
+  BBC_CK(cudaMemsetAsync(g.acc, 0, 128, g.stream));
+  BBC_CK(cudaMemsetAsync(g.queue, 0, 8, g.stream));
+  BBC_CK(cudaEventRecord(g.ev0, g.stream));
+  if (n > 0) {
+    k_ext<T, MINB, MODE><<<blocks, T, smem_bytes, g.stream>>>(P);
+    BBC_CK(cudaGetLastError());
+  }
+  BBC_CK(cudaEventRecord(g.ev1, g.stream));
+  BBC_CK(cudaMemcpyAsync(h_acc, g.acc, 13 * 8, cudaMemcpyDeviceToHost, g.stream));
+  BBC_CK(cudaStreamSynchronize(g.stream));
+  cudaEventElapsedTime(ms, g.ev0, g.ev1);
+  g.last_blocks = blocks;
+  *blocks_out = blocks;
+  return BBC_OK;
+}
+
+int ext_check_opts(const bbc_opts& opts) {
+  if (opts.algo != BBC_ALGO_GBBC && opts.algo != BBC_ALGO_GBBCPP) {
+    set_error("algo must be 0 (G-BBC) or 1 (G-BBC++)");
+    return BBC_ERR_ARG;
+  }
+  const int part_count = opts.part_count <= 0 ? 1 : opts.part_count;
+  if (opts.blocks < 0 || opts.part_index < 0 || opts.part_index >= part_count) {
+    set_error("blocks must be >= 0 and part_index in [0, part_count)");
+    return BBC_ERR_ARG;
+  }
+  return BBC_OK;
+}
+
+void ext_stats(Graph& g, bbc_stats* st, int blocks, float ms) {
+  if (!st) return;
+  std::memset(st, 0, sizeof(*st));
+  unsigned long long* bw = new unsigned long long[blocks];
+  cudaMemcpy(bw, g.block_work, (size_t)blocks * 8, cudaMemcpyDeviceToHost);
+  unsigned long long w = 0;
+  for (int b = 0; b < blocks; ++b) w += bw[b];
+  delete[] bw;
+  st->wedges = w;
+  st->wedges_total = g.w_s;
+  st->w_u = g.w_u;
+  st->w_v = g.w_v;
+  st->anchor_side = g.side;
+  st->blocks = blocks;
+  st->threads = 128;
+  st->tasks = (int32_t)g.n;
+  st->preprocess_ms = g.preprocess_ms;
+  st->count_ms = ms;
+}
+
+}  // namespace
+
+int classify_graph(Graph& g, const bbc_opts* o, uint64_t out[12], bbc_stats* st) {
+  bbc_opts opts{};
+  if (o) opts = *o;
+  if (int rc = ext_check_opts(opts)) return rc;
+  if (g.side != 0) {
+    set_error("classification anchors U-pairs over V-centres (oracle.py:176-178): build the graph with BBC_SIDE_U");
+    return BBC_ERR_ARG;
+  }
+  BBC_CK(cudaSetDevice(g.device));
+  unsigned long long h[13];
+  float ms = 0.f;
+  int blocks = 0;
+  if (int rc = ext_launch<kClassify>(g, opts, 2u, h, &ms, &blocks)) return rc;
+  for (int i = 0; i < 12; ++i) out[i] = h[i];
+  ext_stats(g, st, blocks, ms);
+  return BBC_OK;
+}
+
+int count_2k_graph(Graph& g, int32_t k, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
+  bbc_opts opts{};
+  if (o) opts = *o;
+  if (k < 2) {
+    set_error("k must be >= 2, got " + std::to_string(k));
+    return BBC_ERR_ARG;
+  }
+  if (int rc = ext_check_opts(opts)) return rc;
+  BBC_CK(cudaSetDevice(g.device));
+  unsigned long long h[13];
+  float ms = 0.f;
+  int blocks = 0;
+  if (int rc = ext_launch<kBicliques>(g, opts, (uint32_t)k, h, &ms, &blocks)) return rc;
+  out[0] = h[0];
+  out[1] = h[1];
+  ext_stats(g, st, blocks, ms);
+  if (st) st->balanced_hi = h[1];
+  if (h[1] || h[12]) {
+    set_error("balanced (2,k) count exceeded 64-bit range");
+    return BBC_ERR_OVERFLOW;
+  }
+  return BBC_OK;
+}
+
+}  // namespace bbc

@@ -8,6 +8,7 @@ Reference entry points kept (signatures, argument meaning, errors):
   count_balanced_dynamic(g, blocks, thresholds, mode) tiled.py:182-292    (G-BBC++)
   count_balanced_bruteforce(g) -> (balanced, total)   oracle.py:116-124
   sign_product_total(g)                               oracle.py:127-134
+  classify_butterflies(g) -> ButterflyClassCounts     oracle.py:172-197
 
 plus ``count_signed_butterflies(g, ...) -> (balanced, unbalanced)``, the unbalanced count
 the reference only exposes through its brute-force oracle.
@@ -247,17 +248,22 @@ def count_balanced_2k_serial(g: SignedBipartiteGraph, k: int, anchor_side: Side 
                              sort_neighbors: bool = False, counters: WedgeCounters | None = None) -> int:
     """Balanced (2,k)-biclique count with the size-2 side on ``anchor_side`` (buckets.py:64-154).
 
-    k = 2 (balanced butterflies) runs on the device anchored on ``anchor_side``;
-    ``sort_neighbors`` is accepted (device lists are always rank-sorted).  k > 2 is the
-    next build step and raises NotImplementedError.
+    k = 2 (balanced butterflies) runs the count kernel anchored on ``anchor_side``; k > 2
+    runs the (2,k) kernel (csrc/bbc_ext.cu: per pair C(b1,k) + C(b2,k), buckets.py:146)
+    on the same device CSR.  ``sort_neighbors`` is accepted (device lists are always
+    rank-sorted).  CountOverflowError above 2^64 - 1, like the reference.
     """
     if k < 2:
         raise InvalidKError(f"k must be >= 2, got {k}")
-    if k > 2:
-        raise NotImplementedError("balanced (2,k)-bicliques for k > 2 are not on the device path yet")
     if g.side_count(anchor_side) == 0:
         return 0
-    bal, _, _ = _count(g, _devices(1), _lib.ALGO_GBBCPP, anchor_side)
+    if k > 2:
+        _devices(1)
+        bal, overflow, _ = device_graph(g, 0, anchor_side).count_2k(k)
+        if overflow:
+            raise CountOverflowError(f"balanced (2,{k}) count exceeded 64-bit range")
+    else:
+        bal, _, _ = _count(g, _devices(1), _lib.ALGO_GBBCPP, anchor_side)
     if counters is not None:
         dg = device_graph(g, 0, anchor_side)
         ids, work = dg.task_order(_lib.ALGO_GBBC)
@@ -336,3 +342,70 @@ def sign_product_total(g: SignedBipartiteGraph) -> int:
     """Sum over butterflies of the product of the four signs = balanced - unbalanced."""
     bal, unb = count_signed_butterflies(g)
     return bal - unb
+
+
+@dataclass
+class ButterflyClassCounts:
+    """Six-way split by the two wedges through v1, v2 (endpoints u1, u2) -- the reference's
+    oracle.ButterflyClassCounts (oracle.py:31-64), filled from the device."""
+
+    coherent_pp_pp: int = 0
+    coherent_pp_mm: int = 0
+    coherent_mm_mm: int = 0
+    incoherent_pm_pm: int = 0
+    mixed_pp_pm: int = 0
+    mixed_pm_mm: int = 0
+
+    def total(self) -> int:
+        return (self.coherent_pp_pp + self.coherent_pp_mm + self.coherent_mm_mm
+                + self.incoherent_pm_pm + self.mixed_pp_pm + self.mixed_pm_mm)
+
+    def balanced(self) -> int:
+        """Coherent plus incoherent: exactly the balanced butterflies."""
+        return self.coherent_pp_pp + self.coherent_pp_mm + self.coherent_mm_mm + self.incoherent_pm_pm
+
+    def as_dict(self) -> dict[str, int]:
+        return {
+            "coherent_pp_pp": self.coherent_pp_pp,
+            "coherent_pp_mm": self.coherent_pp_mm,
+            "coherent_mm_mm": self.coherent_mm_mm,
+            "incoherent_pm_pm": self.incoherent_pm_pm,
+            "mixed_pp_pm": self.mixed_pp_pm,
+            "mixed_pm_mm": self.mixed_pm_mm,
+        }
+
+
+def classify_butterflies(g: SignedBipartiteGraph, devices: int = 1, algo: str = "gbbc++") -> ButterflyClassCounts:
+    """Tally the six wedge-pattern classes over all butterflies (oracle.py:172-197).
+
+    Runs the classification kernel (csrc/bbc_ext.cu) on a U-anchored device CSR (the
+    classes pair U vertices over V centres, oracle.py:176-178), with start vertices split
+    over ``devices`` GPUs of this process and the exact sums added.
+    """
+    if devices < 1:
+        raise ValueError(f"devices must be >= 1, got {devices}")
+    code = {"gbbc++": _lib.ALGO_GBBCPP, "gbbc": _lib.ALGO_GBBC}.get(algo)
+    if code is None:
+        raise ValueError(f"unknown algo {algo!r}")
+    if g.u_count == 0 or g.v_count == 0:
+        return ButterflyClassCounts()
+    devs = _devices(devices)
+    graphs = [device_graph(g, d, Side.U) for d in devs]
+    results: list = [None] * len(graphs)
+    errors: list = []
+
+    def run(i: int) -> None:
+        try:
+            results[i] = graphs[i].classify(code, part_index=i, part_count=len(graphs))[0]
+        except BaseException as e:  # re-raised on the caller's thread
+            errors.append(e)
+
+    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(graphs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    total = {k: sum(r[k] for r in results) for k in results[0]}
+    return ButterflyClassCounts(**total)

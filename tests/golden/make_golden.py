@@ -5,6 +5,7 @@ absent on the GPU box, which only reads the committed JSON):
 
     python tests/golden/make_golden.py            # fixtures, corpora, config 1, scaled configs
     python tests/golden/make_golden.py --full 2   # config 2 at full size (long: ~30 min)
+    python tests/golden/make_golden.py --ext      # classification + (2,k) vectors (8(f))
 
 Every count here comes from the reference's own engines (pkg/src/bbcount):
   balanced  = count_balanced_parallel(g, workers)        (buckets.py:213-246)
@@ -157,6 +158,51 @@ def synth_configs(out: dict, which: list[str]) -> None:
         print(f"config {key}: {rec}", flush=True)
 
 
+def extensions(out: dict) -> None:
+    """six-way classification (oracle.classify_butterflies,
+    oracle.py:172-197) and balanced (2,k)-bicliques for k = 3, 4 (count_balanced_2k_serial,
+    buckets.py:64-154, both anchor sides; cross-checked with count_balanced_2k_bruteforce,
+    oracle.py:137-169, where small)."""
+    def b2k(g, brute: bool) -> dict:
+        rec = {}
+        for k in (3, 4):
+            for side in (bbcount.Side.U, bbcount.Side.V):
+                val = bbcount.count_balanced_2k_serial(g, k, side)
+                if brute:
+                    assert bbcount.count_balanced_2k_bruteforce(g, k, side) == val
+                rec[f"k{k}_{side.value}"] = val
+        return rec
+
+    ref_named = {name: None for name in out["named"]}
+    mine = fixtures.named_fixtures()
+    for name in ref_named:
+        if name == "smoke_graph":
+            continue
+        f = mine[name]
+        rec = out["named"][name]
+        g = bbcount.build(f.n_u, f.n_v, list(zip(f.u.tolist(), f.v.tolist(), f.s.tolist())))
+        assert ref_digest(g) == rec["digest"]
+        if g.u_count and g.v_count:
+            rec["b2k"] = b2k(g, brute=g.edge_count <= 400)
+    for name, (seed, count, mu, mv, pe, pp) in fixtures.CORPORA.items():
+        rng = random.Random(seed)
+        ref_graphs = [ref_conftest.random_graph(rng, mu, mv, pe, pp) for _ in range(count)]
+        ext = []
+        for g in ref_graphs:
+            cls = bbcount.classify_butterflies(g).as_dict()
+            ext.append({"classes": cls, "b2k": b2k(g, brute=g.edge_count <= 60)})
+        out.setdefault("corpora_ext", {})[name] = ext
+    for key in ("1@1", "5@small"):
+        cfg = synth.golden_config(key)
+        u, v, s = synth.generate(cfg)
+        g = bbcount.build(cfg.n_u, cfg.n_v, list(zip(u.tolist(), v.tolist(), s.tolist())))
+        t0 = time.time()
+        rec = out["configs"][key]
+        rec["classes"] = bbcount.classify_butterflies(g).as_dict()
+        rec["b2k"] = b2k(g, brute=False)
+        print(f"config {key} extensions in {time.time() - t0:.1f}s: {rec['classes']} {rec['b2k']}", flush=True)
+
+
 def main() -> None:
     path = HERE / "golden.json"
     out = json.loads(path.read_text()) if path.exists() else {}
@@ -164,7 +210,9 @@ def main() -> None:
     out.setdefault("corpora", {})
     out.setdefault("configs", {})
     out["generator"] = "tests/golden/make_golden.py (reference bbcount 0.1.0 at /root/reference/pkg/src)"
-    if "--full" in sys.argv:
+    if "--ext" in sys.argv:
+        extensions(out)
+    elif "--full" in sys.argv:
         cfg_id = int(sys.argv[sys.argv.index("--full") + 1])
         synth_configs(out, [f"{cfg_id}@1"])
     else:
