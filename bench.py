@@ -46,6 +46,7 @@ def parse_args():
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-extensions", action="store_true", help="skip the 8(f) classification / (2,k) timings")
     return p.parse_args()
 
 
@@ -314,11 +315,37 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_port_rate(cfg.n_u, cfg.n_v, u, v, s, args.cpu_seconds)
     g.close()
+    if world == 1 and not args.no_extensions:
+        line["extensions"] = extensions(cfg, du, dv, ds, local)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def extensions(cfg, du, dv, ds, device) -> dict:
+    """SURVEY.md 8(f) rows on the same workload, device-timed (one warm-up + one timed run):
+    six-way classification (U anchors, oracle.py:172-197) and balanced (2,3)-bicliques
+    (count_balanced_2k_serial k = 3, buckets.py:64-154) with the size-2 side V."""
+    from paper_2601_17707_b200 import _lib
+
+    out = {}
+    gu = _lib.DeviceGraph.from_device_ptrs(cfg.n_u, cfg.n_v, cfg.m, du.data_ptr(), dv.data_ptr(), ds.data_ptr(),
+                                           device, _lib.SIDE_U)
+    gu.classify()
+    cls, ms = gu.classify()
+    out["classify"] = {"ms": ms, "wedges": gu.w_s, "wedges_per_s": gu.w_s / (ms * 1e-3), "anchor_side": "U",
+                       "classes": cls}
+    gu.close()
+    gv = _lib.DeviceGraph.from_device_ptrs(cfg.n_u, cfg.n_v, cfg.m, du.data_ptr(), dv.data_ptr(), ds.data_ptr(),
+                                           device, _lib.SIDE_V)
+    gv.count_2k(3)
+    val, ovf, ms = gv.count_2k(3)
+    out["bicliques_k3"] = {"ms": ms, "wedges": gv.w_s, "wedges_per_s": gv.w_s / (ms * 1e-3), "anchor_side": "V",
+                           "count": val, "overflow": ovf}
+    gv.close()
+    return out
 
 
 def ctypes_create(pu, pv, ps, cfg, device):

@@ -38,12 +38,26 @@ def _run(cmd: list[str]) -> None:
 
 
 def build_libbbc(force: bool = False) -> Path:
+    """Each translation unit compiled in parallel (objects under build/), then one link."""
     srcs = sorted(CSRC.glob("bbc_*.cu"))
     deps = srcs + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "bbc.h"]
     if force or _stale(LIBBBC, deps):
+        objdir = ROOT / "build"
+        objdir.mkdir(exist_ok=True)
+        flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", str(ROOT / "include")]
+        procs = []
+        objs = []
+        for src in srcs:
+            obj = objdir / (src.stem + ".o")
+            objs.append(obj)
+            cmd = [NVCC, *flags, "-c", "-o", str(obj), str(src)]
+            print("+", " ".join(cmd), file=sys.stderr)
+            procs.append((subprocess.Popen(cmd), cmd))
+        for p, cmd in procs:
+            if p.wait():
+                raise subprocess.CalledProcessError(p.returncode, cmd)
         tmp = LIBBBC.with_suffix(".so.tmp")
-        _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler",
-              "-fPIC,-O2", "-I", str(ROOT / "include"), "-o", str(tmp), *map(str, srcs)])
+        _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)])
         os.replace(tmp, LIBBBC)
     return LIBBBC
 

@@ -76,7 +76,9 @@ struct OpBiclW16 {
   unsigned long long lo = 0, hi = 0;
   uint32_t ovf = 0;
   __device__ __forceinline__ void add(uint32_t c) {
-    const unsigned long long x = k1 == 1u ? (unsigned long long)c : binom_dev(c, k1);
+    // C(c, k-1) for c >= k-1; closed forms for k = 2, 3 (exact in 64 bits for c < 2^32)
+    const unsigned long long cc = c;
+    const unsigned long long x = k1 == 1u ? cc : k1 == 2u ? (cc * (cc - 1ull)) >> 1 : binom_dev(c, k1);
     if (x == ~0ull) ovf = 1u;
     lo += x;
     hi += (lo < x) ? 1ull : 0ull;

@@ -46,28 +46,47 @@ inline int bits_for(uint64_t x) {
 
 // First failing edge in input order: code = edge * 4 + kind, kind 0 u-range,
 // 1 v-range, 2 sign.  Degrees of valid edges are accumulated.
+__device__ __forceinline__ void validate_edge(int64_t i, int32_t uu, int32_t vv, int32_t ss, int64_t n_u, int64_t n_v,
+                                              unsigned int* __restrict__ deg_u, unsigned int* __restrict__ deg_v,
+                                              unsigned long long* __restrict__ err) {
+  unsigned long long code = ~0ull;
+  if (uu < 0 || uu >= n_u)
+    code = (unsigned long long)i * 4ull;
+  else if (vv < 0 || vv >= n_v)
+    code = (unsigned long long)i * 4ull + 1ull;
+  else if (ss != 1 && ss != -1)
+    code = (unsigned long long)i * 4ull + 2ull;
+  if (code != ~0ull) {
+    atomicMin(err, code);
+  } else {
+    atomicAdd(&deg_u[uu], 1u);
+    atomicAdd(&deg_v[vv], 1u);
+  }
+}
+
+// Four edges per thread with 16-byte loads of u / v and one 4-byte load of signs when the
+// arrays are 16-byte aligned (the tail and unaligned inputs go edge by edge).
 __global__ void k_validate_degrees(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
                                    const int8_t* __restrict__ s, int64_t m, int64_t n_u, int64_t n_v,
                                    unsigned int* __restrict__ deg_u, unsigned int* __restrict__ deg_v,
                                    unsigned long long* __restrict__ err) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t uu = u[i], vv = v[i];
-    int8_t ss = s[i];
-    unsigned long long code = ~0ull;
-    if (uu < 0 || uu >= n_u)
-      code = (unsigned long long)i * 4ull;
-    else if (vv < 0 || vv >= n_v)
-      code = (unsigned long long)i * 4ull + 1ull;
-    else if (ss != 1 && ss != -1)
-      code = (unsigned long long)i * 4ull + 2ull;
-    if (code != ~0ull) {
-      atomicMin(err, code);
-    } else {
-      atomicAdd(&deg_u[uu], 1u);
-      atomicAdd(&deg_v[vv], 1u);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15u) == 0 &&
+                   (reinterpret_cast<uintptr_t>(s) & 3u) == 0;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t m4 = m / 4;
+    for (int64_t q = tid; q < m4; q += nt) {
+      const int4 u4 = reinterpret_cast<const int4*>(u)[q], v4 = reinterpret_cast<const int4*>(v)[q];
+      const int32_t s4 = reinterpret_cast<const int32_t*>(s)[q];
+      validate_edge(4 * q + 0, u4.x, v4.x, (int8_t)(s4 & 0xff), n_u, n_v, deg_u, deg_v, err);
+      validate_edge(4 * q + 1, u4.y, v4.y, (int8_t)((s4 >> 8) & 0xff), n_u, n_v, deg_u, deg_v, err);
+      validate_edge(4 * q + 2, u4.z, v4.z, (int8_t)((s4 >> 16) & 0xff), n_u, n_v, deg_u, deg_v, err);
+      validate_edge(4 * q + 3, u4.w, v4.w, (int8_t)(s4 >> 24), n_u, n_v, deg_u, deg_v, err);
     }
+    done = m4 * 4;
   }
+  for (int64_t i = done + tid; i < m; i += nt) validate_edge(i, u[i], v[i], s[i], n_u, n_v, deg_u, deg_v, err);
 }
 
 // sum C(d, 2) and max d over one degree array
@@ -100,30 +119,32 @@ __global__ void k_scatter_rank(const uint32_t* __restrict__ rank_to_id, int64_t 
     rank[rank_to_id[i]] = (uint32_t)i;
 }
 
-// centre-major key: c << 32 | rank(a) << 1 | neg
+// centre-major key: c << cs | rank(a) << 1 | neg, cs = rank bits + 1 (the radix sort then
+// needs only bits(nc) + cs bits: 40 instead of 52 passes' worth on config 2)
 __global__ void k_centre_keys(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
-                              const int8_t* __restrict__ s, int64_t m, int side,
+                              const int8_t* __restrict__ s, int64_t m, int side, int cs,
                               const uint32_t* __restrict__ rank, unsigned long long* __restrict__ keys) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t a = side == 0 ? (uint32_t)u[i] : (uint32_t)v[i];
     uint32_t c = side == 0 ? (uint32_t)v[i] : (uint32_t)u[i];
-    keys[i] = ((unsigned long long)c << 32) | ((unsigned long long)rank[a] << 1) | (s[i] < 0 ? 1ull : 0ull);
+    keys[i] = ((unsigned long long)c << cs) | ((unsigned long long)rank[a] << 1) | (s[i] < 0 ? 1ull : 0ull);
   }
 }
 
 // adjacency words + duplicate detection + keys for the anchor-major regroup
-__global__ void k_adj_dup(const unsigned long long* __restrict__ keys, int64_t m, int side,
+__global__ void k_adj_dup(const unsigned long long* __restrict__ keys, int64_t m, int side, int cs,
                           const uint32_t* __restrict__ rank_to_id, uint32_t* __restrict__ adj,
                           uint32_t* __restrict__ akey, uint32_t* __restrict__ aval,
                           unsigned long long* __restrict__ dup) {
+  const unsigned long long rmask = (1ull << (cs - 1)) - 1ull;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long k = keys[i];
-    uint32_t r = (uint32_t)((k >> 1) & 0x7fffffffull);
+    uint32_t r = (uint32_t)((k >> 1) & rmask);
     adj[i] = r | ((uint32_t)(k & 1ull) << 31);
     akey[i] = r;
     aval[i] = (uint32_t)i;
     if (i > 0 && (keys[i - 1] >> 1) == (k >> 1)) {
-      unsigned long long c = k >> 32, a = rank_to_id[r];
+      unsigned long long c = k >> cs, a = rank_to_id[r];
       unsigned long long pair = side == 0 ? ((a << 32) | c) : ((c << 32) | a);
       atomicMin(dup, pair);
     }
@@ -132,12 +153,36 @@ __global__ void k_adj_dup(const unsigned long long* __restrict__ keys, int64_t m
 
 // records in anchor-rank order: rec[j] = {(i + 1) | neg << 31, c}; the admitted suffix of
 // centre c's list is [i + 1, coff[c + 1])
-__global__ void k_records(const uint32_t* __restrict__ pos_sorted, const unsigned long long* __restrict__ keys,
-                          int64_t m, uint2* __restrict__ rec) {
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t i = pos_sorted[j];
-    unsigned long long k = keys[i];
-    rec[j] = make_uint2((i + 1u) | ((uint32_t)(k & 1ull) << 31), (uint32_t)(k >> 32));
+// (and awork: the records' admitted wedges coff[c + 1] - (i + 1) summed per anchor rank
+// r = akey[j]; records of one anchor are contiguous, so a warp segmented scan leaves one
+// 64-bit atomic per anchor segment and warp)
+__global__ void k_records(const uint32_t* __restrict__ pos_sorted, const uint32_t* __restrict__ akey,
+                          const unsigned long long* __restrict__ keys, int64_t m, int cs,
+                          const uint32_t* __restrict__ coff, uint2* __restrict__ rec,
+                          unsigned long long* __restrict__ awork) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < m; base += stride) {
+    const int64_t j = base + lane;
+    unsigned long long w = 0;
+    uint32_t r = 0xffffffffu;
+    if (j < m) {
+      const uint32_t i = pos_sorted[j];
+      const unsigned long long k = keys[i];
+      const uint32_t c = (uint32_t)(k >> cs);
+      rec[j] = make_uint2((i + 1u) | ((uint32_t)(k & 1ull) << 31), c);
+      w = coff[c + 1] - (i + 1u);
+      r = akey[j];
+    }
+    // inclusive segmented sum over lanes with equal r (contiguous)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, w, o);
+      const uint32_t ry = __shfl_up_sync(0xffffffffu, r, o);
+      if (lane >= o && ry == r) w += y;
+    }
+    const uint32_t rn = __shfl_down_sync(0xffffffffu, r, 1);
+    if (j < m && (lane == 31 || rn != r)) atomicAdd(&awork[r], w);
   }
 }
 
@@ -197,23 +242,6 @@ __global__ void k_band_table(const uint32_t* __restrict__ adj, const uint32_t* _
       }
     }
     bnd[(size_t)row * nbands + j] = hi;
-  }
-}
-
-// admitted wedges per anchor: one warp per anchor
-__global__ void k_anchor_work(const uint2* __restrict__ rec, const uint32_t* __restrict__ aoff,
-                              const uint32_t* __restrict__ coff, int64_t n, unsigned long long* __restrict__ awork) {
-  int lane = threadIdx.x & 31;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t a = warp; a < n; a += nwarps) {
-    unsigned long long acc = 0;
-    for (uint32_t e = aoff[a] + lane; e < aoff[a + 1]; e += 32) {
-      uint2 r = rec[e];
-      acc += coff[r.y + 1] - (r.x & 0x7fffffffu);
-    }
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) awork[a] = acc;
   }
 }
 
@@ -360,7 +388,8 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
 
   const int deg_bits = std::max(1, bits_for(maxdeg[side]));
   const int rank_bits = std::max(1, bits_for((uint64_t)n));
-  const int key_bits = 32 + std::max(1, bits_for((uint64_t)nc));
+  const int cs = rank_bits + 1;  // centre shift of the centre-major keys
+  const int key_bits = cs + std::max(1, bits_for((uint64_t)nc));
   size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0, t5 = 0, t6 = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, t1, (unsigned int*)nullptr, (unsigned int*)nullptr, (uint32_t*)nullptr,
                                   (uint32_t*)nullptr, (int)n, 0, deg_bits, st);
@@ -388,12 +417,12 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
     BBC_CK(cub::DeviceScan::ExclusiveSum(temp.p, tb, deg_c, g.coff, (int)(nc + 1), st));
   }
   if (m > 0) {
-    k_centre_keys<<<grid_for(m, sms), kThreads, 0, st>>>(du, dv, ds, m, side, rank.as<uint32_t>(),
+    k_centre_keys<<<grid_for(m, sms), kThreads, 0, st>>>(du, dv, ds, m, side, cs, rank.as<uint32_t>(),
                                                          keys_a.as<unsigned long long>());
     size_t tb = t6;
     BBC_CK(cub::DeviceRadixSort::SortKeys(temp.p, tb, keys_a.as<unsigned long long>(),
                                           keys_b.as<unsigned long long>(), (int)m, 0, key_bits, st));
-    k_adj_dup<<<grid_for(m, sms), kThreads, 0, st>>>(keys_b.as<unsigned long long>(), m, side, g.rank_to_id, g.adj,
+    k_adj_dup<<<grid_for(m, sms), kThreads, 0, st>>>(keys_b.as<unsigned long long>(), m, side, cs, g.rank_to_id, g.adj,
                                                      akey_a.as<uint32_t>(), aval_a.as<uint32_t>(), d_err + 1);
     BBC_CK(cudaGetLastError());
     unsigned long long dup = ~0ull;
@@ -408,7 +437,9 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
     tb = t6;
     BBC_CK(cub::DeviceRadixSort::SortPairs(temp.p, tb, akey_a.as<uint32_t>(), akey_b.as<uint32_t>(),
                                            aval_a.as<uint32_t>(), aval_b.as<uint32_t>(), (int)m, 0, rank_bits, st));
-    k_records<<<grid_for(m, sms), kThreads, 0, st>>>(aval_b.as<uint32_t>(), keys_b.as<unsigned long long>(), m, g.rec);
+    BBC_CK(cudaMemsetAsync(g.awork, 0, (size_t)(n + 1) * 8, st));
+    k_records<<<grid_for(m, sms), kThreads, 0, st>>>(aval_b.as<uint32_t>(), akey_b.as<uint32_t>(),
+                                                     keys_b.as<unsigned long long>(), m, cs, g.coff, g.rec, g.awork);
   }
   // anchor offsets from degrees in rank order
   if (n > 0) {
@@ -421,7 +452,7 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
 
   // ---- K5: per-anchor work and the G-BBC++ dispatch order ---------------------------------
   if (n > 0) {
-    k_anchor_work<<<grid_for(n * 32, sms), kThreads, 0, st>>>(g.rec, g.aoff, g.coff, n, g.awork);
+    if (m == 0) BBC_CK(cudaMemsetAsync(g.awork, 0, (size_t)n * 8, st));
     k_iota<<<grid_for(n, sms), kThreads, 0, st>>>(ids.as<uint32_t>(), n);
     // descending work; LSD radix descending sort is stable -> ties in ascending rank
     unsigned long long* work_sorted = keys_a.as<unsigned long long>();
