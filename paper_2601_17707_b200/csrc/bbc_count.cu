@@ -59,7 +59,7 @@ struct Params {
   uint32_t span32;
   uint32_t cap_words;
   int fast;         // 0: always the general banded path (flags bit 0)
-  uint32_t hslots;  // cold-range hash slots (0: no hash round; flags bit 13 enables)
+  uint32_t hash_thr;  // cold range in key-hash rounds when bitmap rounds would average fewer wedges
   uint32_t t16;     // band-table granularity (ranks per column)
   uint32_t bcols8;  // this launch's tile band in table columns (W8 / W16 layouts)
   uint32_t bcols16;
@@ -158,29 +158,6 @@ __device__ __forceinline__ void walk(const Params& P, uint32_t* cnt, const uint3
   }
 }
 
-// Cold-range accumulation in a shared-memory hash table: slot i holds key = rank + 1
-// (0 = empty) in word 2i and the packed u16 positive | negative counts in word 2i + 1;
-// linear probing over K slots; closing inline from the add's return value.
-__device__ __forceinline__ void hash_bump_close(uint32_t* tab, uint32_t K, uint32_t rank, uint32_t par,
-                                                unsigned long long& tb, unsigned long long& tu) {
-  const uint32_t key = rank + 1u;
-  uint32_t h = (uint32_t)(((unsigned long long)(key * 0x9E3779B1u) * K) >> 32);
-  volatile uint32_t* vk = tab;
-  for (;;) {
-    uint32_t k = vk[2u * h];
-    if (k == key) break;
-    if (k == 0u) {
-      k = atomicCAS(&tab[2u * h], 0u, key);
-      if (k == 0u || k == key) break;
-    }
-    h = (h + 1u == K) ? 0u : h + 1u;
-  }
-  const uint32_t sh = par << 4;
-  const uint32_t old = atomicAdd(&tab[2u * h + 1u], 1u << sh);
-  tb += (old >> sh) & 0xffffu;
-  tu += (old >> (sh ^ 16u)) & 0xffffu;
-}
-
 // The tile / bitmap ops address their words from a REBASED shared address: rb = base -
 // (lo_rank / ranks-per-word) * 4 (mod 2^32), so a wedge's word is rb + (rank / per-word) * 4
 // with no subtraction; lo_rank is aligned to the ranks per word (tiles are sized with the
@@ -235,13 +212,32 @@ struct OpTileClose {
   }
 };
 
-// cold-range hash round: key = rank + 1 in word 2i, packed u16 counts in word 2i + 1
-struct OpHash {
-  uint32_t* tab;
-  uint32_t K;
-  unsigned long long *tb, *tu;
+// ---- very wide cold ranges: key hash + repeat queue ------------------------------------
+// When the cold range spans so many ranks that bitmap rounds would hold only a few hundred
+// wedges each (config 4: tens of millions of end-vertex ranks), a round instead covers as
+// many table columns as hold about K / 2 wedges, in a linear-probing hash of K keys
+// (rank + 1, with the parity of the end vertex's FIRST wedge in bit 31).  The first wedge
+// of an end vertex inserts its key; a later one finds it and queues (slot, own parity).
+// After the walk the queue is counted into a parallel array of packed u16 counts and every
+// repeated slot is closed once (first wedge's parity from the key).  The round's wedge
+// count is known before the walk (block scan), so the hash never fills; a queue overflow
+// redoes the round narrower.
+struct OpKeys {
+  uint32_t* keys;
+  uint32_t K, queue, count, Q;
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
-    hash_bump_close(tab, K, w & 0x7fffffffu, (w ^ sg) >> 31, *tb, *tu);
+    const uint32_t key = (w & 0x7fffffffu) + 1u, par = (w ^ sg) >> 31;
+    uint32_t h = (uint32_t)(((unsigned long long)(key * 0x9E3779B1u) * K) >> 32);
+    for (;;) {
+      const uint32_t old = atomicCAS(&keys[h], 0u, key | (par << 31));
+      if (old == 0u) break;
+      if ((old & 0x7fffffffu) == key) {
+        const uint32_t idx = s_atom_add(count, 1u);
+        if (idx < Q) s_st(queue + (idx << 2), h | (par << 31));
+        break;
+      }
+      h = (h + 1u == K) ? 0u : h + 1u;
+    }
   }
   __device__ __forceinline__ void flush() {}
 };
@@ -458,7 +454,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   // columns needed up front are loaded together (one latency)
   const uint32_t c0 = P.phase == 2 ? 0u : col(0u), c1 = col(hstep);
   const uint32_t c2 = P.phase == 1 ? 0u : col(min(hstep + step, ncols));
-  const uint32_t cn = (P.phase == 1 || !(P.hslots || (P.debug & 4))) ? 0u : col(ncols);
+  const uint32_t cn = (P.phase == 1 || !(P.debug & 4)) ? 0u : col(ncols);
   // sub-slices [lo, hi) (positions of two table columns) -> S arrays, block scan;
   // returns total groups, bw = total wedges
   auto setup = [&](uint32_t hi, uint32_t lo, unsigned long long& bw) -> uint32_t {
@@ -523,16 +519,6 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     }
     // no trailing barrier: every caller's next tile use comes after a setup (two barriers)
     // or after the end of the anchor (one barrier)
-  };
-  auto hash_round = [&](uint32_t ngroups, unsigned long long bw) {
-    if ((P.debug & 4096) && threadIdx.x == 0) atomicAdd(P.acc + 7, 1ull);
-    const uint32_t K = min(P.hslots, max(64u, (uint32_t)(2ull * bw + 31ull) & ~31u));
-    OpHash op{S.cnt, K, &tb, &tu};
-    walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
-    __syncthreads();
-    uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
-    for (uint32_t i = threadIdx.x; i < (2u * K + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
-    __syncthreads();
   };
   // band-by-band tile rounds over columns [ca, cb); a band is `step` columns starting at
   // any column (the table has every boundary), the last one truncated at cb
@@ -632,6 +618,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       // the bitmap is no longer read (closing uses the queue's parity bits); the next
       // round's setup barriers order this clearing before its walk
       uint4* c4 = reinterpret_cast<uint4*>(bm);
+#pragma unroll 4
       for (uint32_t i = threadIdx.x; i < span_words / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
       if (P.debug & 4096) {
         if (t0) atomicAdd(P.acc + 4, 1ull);
@@ -656,18 +643,107 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     }
   };
 
-  // cold range: one hash round if it fits; else two-bit bitmap rounds (8x the span of a
+  // cold range in key-hash rounds over adaptive column ranges (see OpKeys): a round aims
+  // at `target` wedges; the first width comes from the cold range's average density
+  auto hash_rounds = [&](unsigned long long wc) {
+    const uint32_t Q = (P.cap_words / 16u) & ~3u;
+    const uint32_t K = ((P.cap_words - Q) / 2u) & ~3u;
+    const uint32_t target = K / 2u;
+    const uint32_t span = ncols - hstep;
+    uint32_t cols = (uint32_t)max(1ull, min((unsigned long long)span, (unsigned long long)target * span / max(wc, 1ull)));
+    uint32_t hi = c1;
+    uint32_t parity = 0;
+    uint32_t* keys = S.cnt;
+    uint32_t* cnts = keys + K;
+    uint32_t* queue = cnts + K;
+    for (uint32_t c = hstep; c < ncols;) {
+      const uint32_t cb = min(c + cols, ncols);
+      const uint32_t lo = col(cb);
+      uint32_t* cnt = S.ins + (parity++ & 1u);
+      if (t0) *cnt = 0u;
+      unsigned long long bw;
+      const uint32_t ng = setup(hi, lo, bw);
+      if (ng == 0u) {
+        hi = lo;
+        c = cb;
+        cols = min(2u * cols, span);
+        continue;
+      }
+      if (bw > target && cols > 1u) {  // too many wedges for the hash: narrower, no walk
+        cols = max(1u, min(cols / 2u, (uint32_t)((unsigned long long)cols * target / bw)));
+        continue;
+      }
+      if (bw > target) {  // a single column denser than the hash: one counter-tile round
+        if (t0) work += bw;
+        tile_round(c, 1u, ng, bw);
+        hi = lo;
+        c = cb;
+        continue;
+      }
+      if ((P.debug & 4096) && t0) atomicAdd(P.acc + 7, 1ull);
+      OpKeys op{keys, K, sptr(queue), sptr(cnt), Q};
+      walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ng, op);
+      __syncthreads();
+      const uint32_t nq = *cnt;
+      const bool ovf = nq > Q;
+      if (nq != 0u && !ovf) {
+        // count the repeats per slot; each entry also takes the first wedge's parity
+        for (uint32_t i = threadIdx.x; i < nq; i += T) {
+          const uint32_t e = queue[i], h = e & 0x7fffffffu;
+          atomicAdd(&cnts[h], (e >> 31) ? 0x10000u : 1u);
+          queue[i] = h | ((keys[h] >> 31) << 30);
+        }
+        __syncthreads();
+        // the first entry of a slot to take its counts closes it
+        for (uint32_t i = threadIdx.x; i < nq; i += T) {
+          const uint32_t e = queue[i];
+          queue[i] = 0u;
+          const uint32_t v = atomicExch(&cnts[e & 0x3fffffffu], 0u);
+          if (v == 0u) continue;
+          const unsigned long long neg = (e >> 30) & 1u;
+          const unsigned long long pc = (v & 0xffffu) + (neg ^ 1ull), qc = (v >> 16) + neg;
+          tb += ((pc * (pc - 1ull)) >> 1) + ((qc * (qc - 1ull)) >> 1);
+          tu += pc * qc;
+        }
+      } else if (ovf) {
+        uint4* q4 = reinterpret_cast<uint4*>(queue);
+        for (uint32_t i = threadIdx.x; i < Q / 4u; i += T) q4[i] = make_uint4(0u, 0u, 0u, 0u);
+      }
+      // keys are no longer read (parities travelled with the queue entries)
+      uint4* k4 = reinterpret_cast<uint4*>(keys);
+#pragma unroll 4
+      for (uint32_t i = threadIdx.x; i < K / 4u; i += T) k4[i] = make_uint4(0u, 0u, 0u, 0u);
+      if (!ovf) {
+        if (t0) work += bw;
+        hi = lo;
+        c = cb;
+        if (2ull * bw < target) cols = min(2u * cols, span);
+      } else if (cols > 1u) {
+        cols = (cols + 1u) / 2u;
+      } else {
+        unsigned long long tbw;
+        const uint32_t tng = setup(hi, lo, tbw);
+        if (t0) work += tbw;
+        if (tng) tile_round(c, 1u, tng, tbw);
+        hi = lo;
+        c = cb;
+      }
+    }
+  };
+
+  // cold range: key-hash rounds when bitmap rounds would average fewer than hash_thr
+  // wedges (very wide, sparse rank ranges); else two-bit bitmap rounds (8x the span of a
   // counter tile) unless counter tiles would average at least bits_thr wedges per round
   // (dense cold ranges, where repeats are common); else counter tiles band by band.
-  if (P.hslots != 0u || P.bm_cols != 0u) {
+  // (flags bit 13 forces hash rounds, bit 9 bitmap rounds, bit 7 disables both)
+  if (P.bm_cols != 0u) {
     // cold wedges: the anchor's work minus the hub band's (a block scan only when the hub
-    // round was skipped or a hash round may need the slices)
+    // round was skipped)
     unsigned long long wc = w_a - hub_w;
-    uint32_t ng = 0;
-    if (P.hslots != 0u || (P.debug & 4)) ng = setup(c1, cn, wc);
-    if (P.hslots != 0u && 3ull * wc <= 2ull * P.hslots) {  // load <= 2/3
-      if (t0) work += wc;
-      if (ng) hash_round(ng, wc);
+    if (P.debug & 4) setup(c1, cn, wc);
+    const unsigned long long bm_rounds = (ncols - hstep + P.bm_cols - 1u) / P.bm_cols;
+    if ((P.debug & 8192) || wc < (unsigned long long)P.hash_thr * bm_rounds) {
+      hash_rounds(wc);
       return;
     }
     const unsigned long long tile_rounds = (ncols - hstep + step - 1u) / step;
@@ -807,9 +883,11 @@ int configure(Graph& g, Launch& L) {
       return configure_t<1024, 1>(g, L);
     default:
       // 128-thread CTAs: 8 per SM (default) or, for experiments (env BBC_MINB), 10 / 12
-      // with fewer registers and smaller tiles
+      // with fewer registers and smaller tiles, or 4 / 6 with larger tiles
       if (g.minb == 12) return configure_t<128, 12>(g, L);
       if (g.minb == 10) return configure_t<128, 10>(g, L);
+      if (g.minb == 6) return configure_t<128, 6>(g, L);
+      if (g.minb == 4) return configure_t<128, 4>(g, L);
       return configure_t<128, 8>(g, L);
   }
 }
@@ -874,8 +952,9 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
 
   // tuning knobs (defaults measured on config 2; env overrides for experiments)
   struct {
-    uint32_t rep_slots = 256, bits_thr = 4096, sweep_min = 2, bm_cols0 = 8;
+    uint32_t rep_slots = 256, bits_thr = 4096, sweep_min = 2, bm_cols0 = 8, hash_thr = 512;
   } tune;
+  if (const char* e = std::getenv("BBC_HASH_THR")) tune.hash_thr = (uint32_t)std::atoi(e);
   if (const char* e = std::getenv("BBC_BM_COLS0")) tune.bm_cols0 = (uint32_t)std::atoi(e);
   if (const char* e = std::getenv("BBC_REP_SLOTS")) tune.rep_slots = (uint32_t)std::atoi(e);
   if (const char* e = std::getenv("BBC_BITS_THR")) tune.bits_thr = (uint32_t)std::atoi(e);
@@ -917,9 +996,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     // ranks < 2^30 (rebased word addressing)
     P.fast = ((opts.flags & 1) || tile_override || g.t16 == 0 || n >= (1u << 30)) ? 0 : 1;
     P.fast_max = two_phase ? (uint32_t)std::min(L.threads, Lc.threads) : (uint32_t)X.threads;
-    // one-round cold hash for light anchors: flags bit 13 (measured slower than bitmap
-    // rounds on config 2 once those had a repeat queue: 17.0 vs 16.4 ms)
-    P.hslots = (opts.flags & 8192) && !(opts.flags & 2) ? (uint32_t)X.cap_words / 2u : 0u;
+    P.hash_thr = (opts.flags & 2) ? 0u : tune.hash_thr;  // flags bit 1: no key-hash rounds
     // cold two-bit bitmap rounds (flags bit 7 disables): the widest round leaves room for
     // a queue of rep_slots repeats (flags bit 8: 16, and rounds start at that width, so
     // that tests exercise the overflow / narrowing path)
