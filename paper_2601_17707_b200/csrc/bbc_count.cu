@@ -444,17 +444,18 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   }
   // column j of this thread's record: first position of its list with rank >= n - j * t16
   // (0 past the last column: start of the list), from the band table or, without one
-  // (end-vertex ranges too wide for a table), by binary search within the admitted suffix
-  auto col = [&](uint32_t j) -> uint32_t {
+  // (end-vertex ranges too wide for a table), by a galloping search down from `from`, a
+  // position known to be at or above it (the previous round's boundary)
+  auto col = [&](uint32_t j, uint32_t from) -> uint32_t {
     if (!mine || j >= P.nbands) return 0u;
     if (row) return __ldg(row + j);
     if (j == 0u) return lend;
-    return lower_bound_rank(P.adj, recx & 0x7fffffffu, lend, (long long)P.n - (long long)j * t16);
+    return lower_bound_gallop(P.adj, recx & 0x7fffffffu, from, (long long)P.n - (long long)j * t16);
   };
   // columns needed up front are loaded together (one latency)
-  const uint32_t c0 = P.phase == 2 ? 0u : col(0u), c1 = col(hstep);
-  const uint32_t c2 = P.phase == 1 ? 0u : col(min(hstep + step, ncols));
-  const uint32_t cn = (P.phase == 1 || !(P.debug & 4)) ? 0u : col(ncols);
+  const uint32_t c0 = P.phase == 2 ? 0u : col(0u, lend), c1 = col(hstep, lend);
+  const uint32_t c2 = P.phase == 1 ? 0u : col(min(hstep + step, ncols), c1);
+  const uint32_t cn = (P.phase == 1 || !(P.debug & 4)) ? 0u : col(ncols, c1);
   // sub-slices [lo, hi) (positions of two table columns) -> S arrays, block scan;
   // returns total groups, bw = total wedges
   auto setup = [&](uint32_t hi, uint32_t lo, unsigned long long& bw) -> uint32_t {
@@ -529,7 +530,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   auto tiles = [&]() {
     uint32_t hi = c1, lo = c2;
     for (uint32_t c = hstep; c < ncols; c += step) {
-      const uint32_t nxt = c + step < ncols ? col(min(c + 2u * step, ncols)) : 0u;
+      const uint32_t nxt = c + step < ncols ? col(min(c + 2u * step, ncols), lo) : 0u;
       unsigned long long bw;
       const uint32_t ng = setup(hi, lo, bw);
       if (t0) work += bw;
@@ -559,7 +560,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     uint32_t parity = 0;  // the queue counter of a round alternates between S.ins[0] / [1]
     for (uint32_t c = hstep; c < ncols;) {
       const uint32_t cb = min(c + cols, ncols);
-      const uint32_t lo = col(cb);
+      const uint32_t lo = col(cb, hi);
       uint32_t* cnt = S.ins + (parity++ & 1u);
       if (t0) *cnt = 0u;  // its last reader finished before the previous round's barriers
       unsigned long long bw;
@@ -658,7 +659,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     uint32_t* queue = cnts + K;
     for (uint32_t c = hstep; c < ncols;) {
       const uint32_t cb = min(c + cols, ncols);
-      const uint32_t lo = col(cb);
+      const uint32_t lo = col(cb, hi);
       uint32_t* cnt = S.ins + (parity++ & 1u);
       if (t0) *cnt = 0u;
       unsigned long long bw;

@@ -31,6 +31,25 @@ __device__ __forceinline__ uint32_t lower_bound_rank(const uint32_t* __restrict_
   return lo;
 }
 
+// The same when the answer is known to be <= hi and usually close to it (successive round
+// boundaries of a record move down its list by a few positions): gallop down from hi,
+// then binary-search the last jump.  Typically one or two loads instead of log2(len).
+__device__ __forceinline__ uint32_t lower_bound_gallop(const uint32_t* __restrict__ adj, uint32_t lo, uint32_t hi,
+                                                       long long x) {
+  if (x <= 0) return lo;
+  uint32_t b = hi, step = 1;  // invariant: every position in [b, hi) has rank >= x
+  while (b > lo) {
+    const uint32_t p = b - min(step, b - lo);
+    if ((long long)(__ldg(adj + p) & 0x7fffffffu) >= x) {
+      b = p;
+      step <<= 1;
+    } else {
+      return lower_bound_rank(adj, p + 1u, b, x);
+    }
+  }
+  return lo;
+}
+
 // Block-wide exclusive scan of one u32 per thread fused with a u64 sum, with ONE barrier:
 // each warp publishes its totals, then every warp scans the (<= 32) warp totals itself.
 // The totals are double-buffered by `buf` (callers alternate it), since consecutive scans

@@ -13,6 +13,7 @@ p.add_argument("keys", nargs="+", help="config keys like 3@1, 4@0.25, 5@1")
 p.add_argument("--reps", type=int, default=2)
 p.add_argument("--flags", type=int, default=0)
 p.add_argument("--algo", type=int, default=1)
+p.add_argument("--extra-flags", type=int, nargs="*", help="time each of these flag sets in turn")
 a = p.parse_args()
 for key in a.keys:
     cfg = synth.golden_config(key)
@@ -22,8 +23,13 @@ for key in a.keys:
     t0 = time.time()
     g = _lib.DeviceGraph.from_host(cfg.n_u, cfg.n_v, u, v, s)
     tb = time.time() - t0
-    for _ in range(a.reps):
-        r = g.count(a.algo, flags=a.flags)
+    for f in a.extra_flags or [a.flags]:
+        for _ in range(a.reps):
+            r = g.count(a.algo, flags=f)
+        if len(a.extra_flags or []) > 1:
+            print(f"  flags {f}: count_ms={r.count_ms:.2f} W={r.wedges:.4e}", flush=True)
+        if f & _lib.FLAG_ROUNDS:
+            print("  rounds", g.round_counters(), flush=True)
     print(f"{key} {cfg.name}: m={cfg.m} side={'UV'[g.anchor_side]} W={r.wedges_total:.4e} bal={r.balanced} "
           f"unb={r.unbalanced} gen={tg:.1f}s build={tb:.2f}s prep_ms={r.preprocess_ms:.1f} count_ms={r.count_ms:.2f} "
           f"rate={r.wedges_total / max(r.count_ms, 1e-6) * 1e3:.3e}/s", flush=True)
