@@ -10,8 +10,6 @@ import sys
 from collections import defaultdict
 from pathlib import Path
 
-src_csv = sys.argv[1]
-top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 _defs: dict[str, list] = {}
 
 
@@ -37,24 +35,32 @@ def region(path: str, ln: int) -> str:
     return f"{Path(path).name}:{name}"
 
 
-rows = list(csv.reader(open(src_csv)))
-inst, samp = defaultdict(int), defaultdict(int)
-cur = None
-for r in rows:
-    if len(r) >= 2 and r[0] in ("File Path", "File Name"):
-        cur = r[1]
-        continue
-    if not r or r[0] == "Line No" or len(r) < 8 or r[2] != "-" or not cur:
-        continue
-    try:
-        ln = int(r[0])
-        s, n = int(r[4] or 0), int(r[7] or 0)
-    except ValueError:
-        continue
-    key = region(cur, ln)
-    inst[key] += n
-    samp[key] += s
-ti, ts = sum(inst.values()) or 1, sum(samp.values()) or 1
-print(f"total warp instructions {ti:.4g}, samples {ts}")
-for k in sorted(inst, key=lambda k: -inst[k])[:top]:
-    print(f"{k:40s} inst {100 * inst[k] / ti:5.1f}%  samples {100 * samp[k] / ts:5.1f}%")
+def regions(rows: list) -> tuple[dict, dict]:
+    """(instructions, stall samples) per file:region from the rows of a source page."""
+    inst, samp = defaultdict(int), defaultdict(int)
+    cur = None
+    for r in rows:
+        if len(r) >= 2 and r[0] in ("File Path", "File Name"):
+            cur = r[1]
+            continue
+        if not r or r[0] == "Line No" or len(r) < 8 or r[2] != "-" or not cur:
+            continue
+        try:
+            ln = int(r[0])
+            s, n = int(r[4] or 0), int(r[7] or 0)
+        except ValueError:
+            continue
+        key = region(cur, ln)
+        inst[key] += n
+        samp[key] += s
+    return inst, samp
+
+
+if __name__ == "__main__":
+    src_csv = sys.argv[1]
+    top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+    inst, samp = regions(list(csv.reader(open(src_csv))))
+    ti, ts = sum(inst.values()) or 1, sum(samp.values()) or 1
+    print(f"total warp instructions {ti:.4g}, samples {ts}")
+    for k in sorted(inst, key=lambda k: -inst[k])[:top]:
+        print(f"{k:40s} inst {100 * inst[k] / ti:5.1f}%  samples {100 * samp[k] / ts:5.1f}%")

@@ -13,6 +13,7 @@ import csv
 import io
 import json
 import subprocess
+import sys
 from pathlib import Path
 
 WANT = {
@@ -56,19 +57,28 @@ def raw_metrics(rep: str) -> list[dict]:
     return launches
 
 
-def hot_lines(rep: str, top: int = 12) -> list[dict]:
+def hot_lines(rep: str, top: int = 12) -> tuple[list[dict], dict]:
+    """Top source lines by stall samples (all files) and instructions / samples per region."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    try:
-        hdr = next(r for r in rows if r and r[0] == "Line No")
-    except StopIteration:
-        return []
-    ix = {h: i for i, h in enumerate(hdr)}
-    stall_cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
-    lines = []
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    import ncu_regions
+
+    inst, samp = ncu_regions.regions(rows)
+    ti, ts = sum(inst.values()) or 1, sum(samp.values()) or 1
+    regs = {k: {"inst_pct": round(100 * inst[k] / ti, 1), "samples_pct": round(100 * samp[k] / ts, 1)}
+            for k in sorted(inst, key=lambda k: -inst[k])[:20]}
+    lines, cur, ix, stall_cols = [], None, None, []
     for r in rows:
-        if len(r) != len(hdr) or r[0] == "Line No" or r[2] != "-":
+        if len(r) >= 2 and r[0] in ("File Path", "File Name"):
+            cur = Path(r[1]).name
+            continue
+        if r and r[0] == "Line No":
+            ix = {h: i for i, h in enumerate(r)}
+            stall_cols = [h for h in r if h.startswith("stall_") and "Not Issued" not in h]
+            continue
+        if ix is None or len(r) != len(ix) or r[2] != "-":
             continue
         try:
             s = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
@@ -76,12 +86,10 @@ def hot_lines(rep: str, top: int = 12) -> list[dict]:
         except ValueError:
             continue
         st = sorted(((int(r[ix[c]] or 0), c[6:]) for c in stall_cols), reverse=True)[:2]
-        lines.append((s, n, int(r[0]), r[1].strip()[:90], st))
-    ts = sum(x[0] for x in lines) or 1
-    ti = sum(x[1] for x in lines) or 1
-    return [{"line": ln, "samples_pct": round(100 * s / ts, 1), "inst_pct": round(100 * n / ti, 1), "source": src,
-             "stalls": {k: round(100 * c / max(s, 1)) for c, k in st}}
-            for s, n, ln, src, st in sorted(lines, reverse=True)[:top]]
+        lines.append((s, n, f"{cur}:{r[0]}", r[1].strip()[:90], st))
+    return ([{"line": ln, "samples_pct": round(100 * s / ts, 1), "inst_pct": round(100 * n / ti, 1), "source": src,
+              "stalls": {k: round(100 * c / max(s, 1)) for c, k in st}}
+             for s, n, ln, src, st in sorted(lines, reverse=True)[:top]], regs)
 
 
 def main():
@@ -104,7 +112,7 @@ def main():
         summary["achieved_algorithmic_gbs"] = alg / k["duration"] / 1e9
         summary["frac_of_measured_hbm_peak"] = summary["achieved_algorithmic_gbs"] / a.peak_gbs
         summary["wedges_per_s_under_profiler"] = a.wedges / k["duration"]
-    summary["hot_lines"] = hot_lines(a.report)
+    summary["hot_lines"], summary["regions"] = hot_lines(a.report)
     Path(a.out).write_text(json.dumps(summary, indent=1) + "\n")
     print(json.dumps({x: summary.get(x) for x in ("kernel", "traffic_bytes", "achieved_algorithmic_gbs",
                                                     "frac_of_measured_hbm_peak")}, indent=1))
