@@ -38,7 +38,7 @@ namespace bbc {
 namespace {
 
 
-enum Mode { kDense = 0, kSparse = 1, kZero = 2 };
+enum Mode { kDense = 0, kSparse = 1 };
 
 struct Params {
   const uint32_t* __restrict__ adj;
@@ -78,86 +78,6 @@ struct Params {
   unsigned long long* block_work;
 };
 
-template <int W>
-__device__ __forceinline__ void bump(uint32_t* cnt, uint32_t rel, uint32_t par) {
-  if (W == 8) {
-    atomicAdd(&cnt[rel >> 1], 1u << (((rel & 1u) << 4) | (par << 3)));
-  } else if (W == 16) {
-    atomicAdd(&cnt[rel], 1u << (par << 4));
-  } else {
-    atomicAdd(&cnt[2u * rel + par], 1u);
-  }
-}
-
-template <int W>
-__device__ __forceinline__ void bump_close(uint32_t* cnt, uint32_t rel, uint32_t par, unsigned long long& tb,
-                                           unsigned long long& tu) {
-  if (W == 8) {
-    const uint32_t sh = ((rel & 1u) << 4) | (par << 3);
-    const uint32_t old = atomicAdd(&cnt[rel >> 1], 1u << sh);
-    tb += (old >> sh) & 0xffu;
-    tu += (old >> (sh ^ 8u)) & 0xffu;
-  } else {
-    const uint32_t sh = par << 4;
-    const uint32_t old = atomicAdd(&cnt[rel], 1u << sh);
-    tb += (old >> sh) & 0xffffu;
-    tu += (old >> (sh ^ 16u)) & 0xffffu;
-  }
-}
-
-// Walk the int4 groups of the batch's sub-slices, one group per thread.  Consecutive
-// threads take consecutive groups of the same record (coalesced 512 B per warp).
-template <int T, int W, int M>
-__device__ __forceinline__ void walk(const Params& P, uint32_t* cnt, const uint32_t* s_lo, const uint32_t* s_hi,
-                                     const uint32_t* s_pfx, int nb, uint32_t ngroups, uint32_t lo_rank,
-                                     unsigned long long& tb, unsigned long long& tu) {
-  const uint4* adj4 = reinterpret_cast<const uint4*>(P.adj);
-  // two groups per thread per iteration, both loads in flight before either is used
-  for (uint32_t g0 = threadIdx.x; g0 < ngroups; g0 += 2 * T) {
-    uint4 q[2];
-    uint32_t lo[2], hi[2], sg[2], p0[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const uint32_t g = g0 + (uint32_t)i * T;
-      lo[i] = 1u;
-      hi[i] = 0u;
-      sg[i] = 0u;
-      p0[i] = 0u;
-      q[i] = make_uint4(0u, 0u, 0u, 0u);
-      if (g < ngroups) {
-        const int k = find_record(s_pfx, nb, g);
-        const uint32_t lox = s_lo[k];
-        lo[i] = lox & 0x7fffffffu;
-        sg[i] = lox & 0x80000000u;
-        hi[i] = s_hi[k];
-        const uint32_t grp = (lo[i] >> 2) + (g - s_pfx[k]);
-        p0[i] = grp << 2;
-        q[i] = ld_stream(adj4 + grp);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const uint32_t wv[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t p = p0[i] + (uint32_t)j;
-        if (p >= lo[i] && p < hi[i]) {
-          const uint32_t word = wv[j];
-          const uint32_t rel = (word & 0x7fffffffu) - lo_rank;
-          const uint32_t par = (word ^ sg[i]) >> 31;  // 1: asymmetric (negative) wedge
-          if (M == kDense) {
-            bump<W>(cnt, rel, par);
-          } else if (M == kSparse) {
-            bump_close<W>(cnt, rel, par, tb, tu);
-          } else {
-            cnt[W == 8 ? (rel >> 1) : rel] = 0u;
-          }
-        }
-      }
-    }
-  }
-}
-
 // The tile / bitmap ops address their words from a REBASED shared address: rb = base -
 // (lo_rank / ranks-per-word) * 4 (mod 2^32), so a wedge's word is rb + (rank / per-word) * 4
 // with no subtraction; lo_rank is aligned to the ranks per word (tiles are sized with the
@@ -173,6 +93,15 @@ struct OpTileDense {
       s_red_add(rb + ((w << 1) & 0xfffffffcu), 1u << (((w & 1u) << 4) | ((v >> 28) & 8u)));
     else
       s_red_add(rb + ((w << 2) & 0xfffffffcu), 1u << ((v >> 27) & 16u));
+  }
+  __device__ __forceinline__ void flush() {}
+};
+
+// W32 tile: separate u32 positive / negative words per end vertex; rb rebased by lo_rank * 8
+struct OpTileDense32 {
+  uint32_t rb;
+  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
+    s_red_add(rb + (w << 3) + (((w ^ sg) >> 29) & 4u), 1u);
   }
   __device__ __forceinline__ void flush() {}
 };
@@ -344,14 +273,17 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
   const uint32_t step = W == 8 ? 2u : 1u;  // table columns per band
   const bool table = P.bnd != nullptr && W != 32;
   const uint32_t nbands_u = (P.n - 1u - r) / span + 1u;  // bands 0..nbands_u-1 hold ranks > r
-  const bool multi = (re - rb) > (uint32_t)T;
+  const uint32_t nbatch = (re - rb + T - 1u) / (uint32_t)T;
   uint32_t scan_buf = 0;  // alternates the scan's total buffers
   for (uint32_t b = 0; b < nbands_u; ++b) {
     const long long top = (long long)P.n - (long long)b * span;
     const long long bot = top - (long long)span;
-    const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
+    // lo_rank aligned to the ranks per word (W8: 2) for the rebased ops
+    const uint32_t lo_rank = (bot > 0 ? (uint32_t)bot : 0u) & (W == 8 ? ~1u : ~0u);
     const uint32_t band_span = (uint32_t)(top - (long long)lo_rank);
     const uint32_t band_words = W == 8 ? (band_span + 1u) / 2u : (W == 16 ? band_span : 2u * band_span);
+    const uint32_t base =
+        sptr(S.cnt) - (W == 8 ? (lo_rank >> 1) << 2 : (W == 16 ? lo_rank << 2 : lo_rank << 3));
     int mode = -1;
     unsigned long long band_w = 0;
     for (uint32_t b0 = rb; b0 < re; b0 += T) {
@@ -376,7 +308,7 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
         lo = max(lo, begin);
         hi = max(hi, lo);
         if (hi > lo) {
-          ng = ((hi + 3u) >> 2) - (lo >> 2);
+          ng = unit_count(lo, hi);
           myw = hi - lo;
         }
         S.lo[threadIdx.x] = lo | (rr.x & 0x80000000u);
@@ -389,20 +321,36 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
       __syncthreads();
       work += myw;
       band_w += bw;
-      // several record batches, or a W32 tile, are always closed by the sweep
-      if (mode < 0) mode = (W == 32 || multi || bw >= band_words) ? kDense : kSparse;
-      if (ngroups == 0) continue;
-      if (mode == kDense) {
-        walk<T, W, kDense>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
-      } else {
-        walk<T, W, kSparse>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
-        __syncthreads();
-        walk<T, W, kZero>(P, S.cnt, S.lo, S.hi, S.pfx, nb, ngroups, lo_rank, tb, tu);
+      // the closing of a band is chosen once, from its first batch: the sweep when the band
+      // will hold >= sweep_min wedges per counter word (and always for W32), else inline
+      // closing from the atomics' return values and a vector clear
+      if (mode < 0)
+        mode = (W == 32 || bw * nbatch >= (unsigned long long)P.sweep_min * band_words || (P.debug & 2048)) ? kDense
+                                                                                                          : kSparse;
+      if (ngroups) {
+        if (mode == kDense) {
+          if (W == 32) {
+            OpTileDense32 op{base};
+            walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+          } else {
+            OpTileDense<W> op{base};
+            walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+          }
+        } else {
+          OpTileClose<W == 32 ? 16 : W, false> op{base, &tb, &tu};
+          walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+        }
       }
-      __syncthreads();
+      __syncthreads();  // the next batch overwrites the record arrays
     }
-    if (mode == kDense && band_w > 0) {
-      sweep<T, W>(S.cnt, band_words, tb, tu);
+    if (band_w > 0) {
+      if (mode == kDense) {
+        sweep<T, W>(S.cnt, band_words, tb, tu);
+      } else {
+        uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
+#pragma unroll 4
+        for (uint32_t i = threadIdx.x; i < (band_words + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+      }
       __syncthreads();
     }
   }
@@ -465,7 +413,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       lo = max(lo, recx & 0x7fffffffu);
       hi = max(hi, lo);
       if (hi > lo) {
-        ng = ((hi + 3u) >> 2) - (lo >> 2);
+        ng = unit_count(lo, hi);
         myw = hi - lo;
       }
       S.lo[threadIdx.x] = lo | (recx & 0x80000000u);
@@ -492,13 +440,13 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     const uint32_t band_span = (uint32_t)(top - (long long)lo_rank);
     const uint32_t band_words = W == 8 ? (band_span + 1u) / 2u : band_span;
     const uint32_t base = sptr(S.cnt) - (W == 8 ? (lo_rank >> 1) << 2 : lo_rank << 2);
-    if (ngroups <= 2u * T) {
-      // at most one pair of groups per thread: close inline and zero the touched words
+    if (ngroups <= (uint32_t)T) {
+      // at most one chunk per thread: close inline and zero the touched words
       // from registers (no second pass over the tile or the adjacency)
       OpTileClose<W, true> op{base, &tb, &tu};
 #pragma unroll
       for (int j = 0; j < 8; ++j) op.touched[j] = 0xffffffffu;
-      walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+      walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < 8; ++j)
@@ -507,14 +455,14 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       // medium rounds: inline closing, then the tile is cleared with vector stores (a
       // closing sweep costs ~9 instructions per counter word, inline closing ~4 per wedge)
       OpTileClose<W, false> op{base, &tb, &tu};
-      walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+      walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
       uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
       for (uint32_t i = threadIdx.x; i < (band_words + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
     } else {
       // dense rounds: no-return increments and the shared-memory closing sweep
       OpTileDense<W> op{base};
-      walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+      walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
       sweep<T, W>(S.cnt, band_words, tb, tu);
     }
@@ -582,7 +530,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       uint32_t* keys = queue + Q;
       uint32_t* vals = keys + K;
       OpBits op{sptr(bm) - ((lo_rank >> 4) << 2), sptr(queue), sptr(cnt), Q};
-      walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ng, op);
+      walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ng, op);
       __syncthreads();
       const uint32_t nq = *cnt;
       const bool ovf = nq > Q;
@@ -683,7 +631,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       }
       if ((P.debug & 4096) && t0) atomicAdd(P.acc + 7, 1ull);
       OpKeys op{keys, K, sptr(queue), sptr(cnt), Q};
-      walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ng, op);
+      walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ng, op);
       __syncthreads();
       const uint32_t nq = *cnt;
       const bool ovf = nq > Q;

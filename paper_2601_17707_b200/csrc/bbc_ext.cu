@@ -183,7 +183,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
         const uint32_t lo = lower_bound_rank(P.adj, begin, hi, bot);
         carry = lo;
         if (hi > lo) {
-          ng = ((hi + 3u) >> 2) - (lo >> 2);
+          ng = unit_count(lo, hi);
           myw = hi - lo;
         }
         S.lo[threadIdx.x] = lo | (rr.x & 0x80000000u);
@@ -203,13 +203,13 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
             OpBiclW16 op;
             op.rb = base - (lo_rank << 2);
             op.k1 = P.k1;
-            walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+            walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
             x = op;
           } else {
             OpBiclW32 op;
             op.rb = base - (lo_rank << 3);
             op.k1 = P.k1;
-            walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+            walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
             x = op;
           }
           add128(acc[0], acc[1], x.lo);
@@ -218,7 +218,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
         } else if (!wide) {
           OpClsC10 op;
           op.rb = base - (lo_rank << 2);
-          walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+          walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
           part[0] += op.c0;
           part[1] += op.c1;
           part[2] += op.c2;
@@ -227,7 +227,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
           part[5] += op.c5;
         } else {
           OpClsC32 op{base - lo_rank * 12u};
-          walk_pairs<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+          walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
         }
       }
       __syncthreads();  // the next batch overwrites the record arrays

@@ -140,49 +140,44 @@ __device__ __forceinline__ void s_st(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// valid slots (bits 0..3) of the int4 group starting at word position p0 for [lo, hi)
-__device__ __forceinline__ uint32_t slot_mask(uint32_t p0, uint32_t lo, uint32_t hi) {
-  const int a = max((int)(lo - p0), 0);
-  const int b = min((int)(hi - p0), 4);
-  return b <= a ? 0u : (((1u << b) - 1u) & (0xfu << a));
+// 256-bit streaming load (sm_100: LDG.E.NA.ENL2.256), no L1 allocation
+__device__ __forceinline__ void ld_stream8(const uint32_t* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
 }
 
-// Walk the int4 groups of the round's sub-slices, a PAIR of consecutive groups per thread
-// per iteration (one record search per pair; the second group usually lies in the same
-// record).  Both loads are issued before either group is processed.  op.wedge(word,
-// sign, slot) runs for every valid wedge; op.flush() after each pair.
+// The walk unit: an aligned 32-byte chunk of 8 adjacency words.  A sub-slice [lo, hi)
+// covers chunks lo / 8 .. (hi - 1) / 8.  (adj is 256-byte aligned and padded by 8 words.)
+__device__ __forceinline__ uint32_t unit_count(uint32_t lo, uint32_t hi) { return ((hi + 7u) >> 3) - (lo >> 3); }
+
+// valid slots (bits 0..7) of the chunk starting at word position p0 for [lo, hi)
+__device__ __forceinline__ uint32_t slot_mask8(uint32_t p0, uint32_t lo, uint32_t hi) {
+  const int a = max((int)(lo - p0), 0);
+  const int b = min((int)(hi - p0), 8);
+  return b <= a ? 0u : (((1u << b) - 1u) & (0xffu << a));
+}
+
+// Walk the 32-byte chunks of the round's sub-slices, one chunk (8 wedges) per thread per
+// iteration: one fixed-depth record search and one 256-bit load per chunk; consecutive
+// threads take consecutive chunks of a record (a warp reads 1 KB contiguous).
+// op.wedge(word, sign, slot) runs for every valid wedge; op.flush() after each chunk.
 template <int T, class Op>
-__device__ __forceinline__ void walk_pairs(const uint32_t* adj, const uint32_t* s_lo, const uint32_t* s_hi,
-                                           const uint32_t* s_pfx, int nb, uint32_t ngroups, Op& op) {
-  const uint4* adj4 = reinterpret_cast<const uint4*>(adj);
-  const uint32_t npairs = (ngroups + 1u) >> 1;
-  for (uint32_t gp = threadIdx.x; gp < npairs; gp += T) {
-    const uint32_t g = gp << 1;
+__device__ __forceinline__ void walk_chunks(const uint32_t* adj, const uint32_t* s_lo, const uint32_t* s_hi,
+                                            const uint32_t* s_pfx, int nb, uint32_t nunits, Op& op) {
+  for (uint32_t g = threadIdx.x; g < nunits; g += T) {
     const int k = find_record_fixed<T>(s_pfx, nb, g);
-    const uint32_t lx0 = s_lo[k], hi0 = s_hi[k];
-    const uint32_t lo0 = lx0 & 0x7fffffffu, sg0 = lx0 & 0x80000000u;
-    const uint32_t grp0 = (lo0 >> 2) + (g - s_pfx[k]);
-    const bool has1 = g + 1u < ngroups;
-    uint32_t lo1 = lo0, hi1 = hi0, sg1 = sg0, grp1 = grp0 + 1u;
-    if (has1 && k + 1 < nb && s_pfx[k + 1] <= g + 1u) {
-      int k1 = k + 1;
-      while (k1 + 1 < nb && s_pfx[k1 + 1] <= g + 1u) ++k1;
-      const uint32_t lx1 = s_lo[k1];
-      lo1 = lx1 & 0x7fffffffu;
-      sg1 = lx1 & 0x80000000u;
-      hi1 = s_hi[k1];
-      grp1 = (lo1 >> 2) + (g + 1u - s_pfx[k1]);
-    }
-    const uint4 q0 = ld_stream(adj4 + grp0);
-    const uint4 q1 = has1 ? ld_stream(adj4 + grp1) : make_uint4(0u, 0u, 0u, 0u);
-    const uint32_t m = slot_mask(grp0 << 2, lo0, hi0) | (has1 ? slot_mask(grp1 << 2, lo1, hi1) << 4 : 0u);
-    const uint32_t wv[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    const uint32_t lx = s_lo[k], hi = s_hi[k];
+    const uint32_t lo = lx & 0x7fffffffu, sg = lx & 0x80000000u;
+    const uint32_t p0 = ((lo >> 3) + (g - s_pfx[k])) << 3;
+    uint32_t wv[8];
+    ld_stream8(adj + p0, wv);
+    const uint32_t m = slot_mask8(p0, lo, hi);
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      if (m & (1u << j)) op.wedge(wv[j], j < 4 ? sg0 : sg1, j);
+      if (m & (1u << j)) op.wedge(wv[j], sg, j);
     op.flush();
   }
 }
-
 
 }  // namespace bbc
