@@ -45,6 +45,7 @@ def build_libbbc(force: bool = False) -> Path:
         objdir = ROOT / "build"
         objdir.mkdir(exist_ok=True)
         flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", str(ROOT / "include")]
+        flags += os.environ.get("BBC_NVCC_EXTRA", "").split()  # experiments only (e.g. -DBBC_WALK2)
         procs = []
         objs = []
         for src in srcs:
