@@ -187,12 +187,14 @@ struct OpKeys {
 struct OpBits {
   uint32_t rb, queue, count, Q;
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
-    const uint32_t i = w & 15u;                     // bit i: seen, bit 16 + i: parity
-    const uint32_t v = w ^ sg;
-    const uint32_t one = 1u << i;
-    const uint32_t old = s_atom_or(rb + ((w >> 2) & 0x0ffffffcu), one | ((v >> 31) << (16u + i)));
-    if (old & one) {
-      const uint32_t cneg = (v >> 31) & (old >> (16u + i));
+    // bits = (1 | neg << 16) << i with neg = parity of (w ^ sg); (sg >> 15) | 1 is the same
+    // for the whole chunk, so per wedge: shift, one LOP3, shift
+    const uint32_t i = w & 15u;
+    const uint32_t bits = (((w >> 15) & 0x10000u) ^ ((sg >> 15) | 1u)) << i;
+    const uint32_t old = s_atom_or(rb + ((w >> 2) & 0x0ffffffcu), bits);
+    if (old & bits & 0xffffu) {  // seen before: a repeat
+      // counted as negative only if it is negative and the parity bit was already set
+      const uint32_t cneg = ((old & bits) >> 16) != 0u;
       const uint32_t idx = s_atom_add(count, 1u);
       if (idx < Q) s_st(queue + (idx << 2), (w & 0x7fffffffu) | (cneg << 31));
     }
@@ -680,7 +682,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     }
   };
 
-  // cold range: key-hash rounds when bitmap rounds would average fewer than hash_thr
+  // cold range: key-hash rounds when bitmap rounds would average fewer than hash_thr (256)
   // wedges (very wide, sparse rank ranges); else two-bit bitmap rounds (8x the span of a
   // counter tile) unless counter tiles would average at least bits_thr wedges per round
   // (dense cold ranges, where repeats are common); else counter tiles band by band.
@@ -901,7 +903,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
 
   // tuning knobs (defaults measured on config 2; env overrides for experiments)
   struct {
-    uint32_t rep_slots = 256, bits_thr = 4096, sweep_min = 2, bm_cols0 = 8, hash_thr = 512;
+    uint32_t rep_slots = 256, bits_thr = 4096, sweep_min = 2, bm_cols0 = 8, hash_thr = 256;
   } tune;
   if (const char* e = std::getenv("BBC_HASH_THR")) tune.hash_thr = (uint32_t)std::atoi(e);
   if (const char* e = std::getenv("BBC_BM_COLS0")) tune.bm_cols0 = (uint32_t)std::atoi(e);

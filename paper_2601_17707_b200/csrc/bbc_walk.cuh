@@ -166,7 +166,11 @@ template <int T, class Op>
 __device__ __forceinline__ void walk_chunks(const uint32_t* adj, const uint32_t* s_lo, const uint32_t* s_hi,
                                             const uint32_t* s_pfx, int nb, uint32_t nunits, Op& op) {
   for (uint32_t g = threadIdx.x; g < nunits; g += T) {
-    const int k = find_record_fixed<T>(s_pfx, nb, g);
+    // search depth by the batch's record count (block-uniform branch): most anchors have
+    // few records
+    const int k = nb <= 32 ? find_record_fixed<32>(s_pfx, nb, g)
+                           : (nb <= 64 || T <= 64 ? find_record_fixed<(T < 64 ? T : 64)>(s_pfx, nb, g)
+                                                  : find_record_fixed<T>(s_pfx, nb, g));
     const uint32_t lx = s_lo[k], hi = s_hi[k];
     const uint32_t lo = lx & 0x7fffffffu, sg = lx & 0x80000000u;
     const uint32_t p0 = ((lo >> 3) + (g - s_pfx[k])) << 3;
