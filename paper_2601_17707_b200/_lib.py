@@ -182,11 +182,11 @@ class DeviceGraph:
                    "mixed_pm_mm")
 
     def classify(self, algo: int = ALGO_GBBCPP, blocks: int = 0, part_index: int = 0,
-                 part_count: int = 1) -> tuple[dict[str, int], float]:
+                 part_count: int = 1, flags: int = 0) -> tuple[dict[str, int], float]:
         """Six-way classification (needs a U-anchored handle): (as_dict() counts, device ms)."""
         if self._h is None:
             raise DeviceError("graph handle already closed")
-        o = Opts(algo=algo, blocks=blocks, part_index=part_index, part_count=part_count)
+        o = Opts(algo=algo, blocks=blocks, part_index=part_index, part_count=part_count, flags=flags)
         out = (ctypes.c_uint64 * 12)()
         st = Stats()
         rc = load().bbc_classify(self._h, ctypes.byref(o), out, ctypes.byref(st))
@@ -196,12 +196,12 @@ class DeviceGraph:
                 float(st.count_ms))
 
     def count_2k(self, k: int, algo: int = ALGO_GBBCPP, blocks: int = 0, part_index: int = 0,
-                 part_count: int = 1) -> tuple[int, bool, float]:
+                 part_count: int = 1, flags: int = 0) -> tuple[int, bool, float]:
         """Balanced (2,k)-bicliques with the size-2 side = this handle's anchor side:
         (count, overflowed past 2^64 - 1, device ms)."""
         if self._h is None:
             raise DeviceError("graph handle already closed")
-        o = Opts(algo=algo, blocks=blocks, part_index=part_index, part_count=part_count)
+        o = Opts(algo=algo, blocks=blocks, part_index=part_index, part_count=part_count, flags=flags)
         out = (ctypes.c_uint64 * 2)()
         st = Stats()
         rc = load().bbc_count_2k(self._h, k, ctypes.byref(o), out, ctypes.byref(st))

@@ -42,6 +42,9 @@ struct ExtParams {
   const uint32_t* __restrict__ aoff;
   const unsigned long long* __restrict__ awork;
   const uint32_t* __restrict__ order;
+  const uint32_t* __restrict__ bnd;   // band table (nullptr: searches only)
+  const uint32_t* __restrict__ brow;
+  uint32_t nbands, t16;
   uint32_t n, ntasks, part_index, part_count;
   uint32_t cap_words;
   uint32_t k1;  // (2,k): k - 1
@@ -129,6 +132,28 @@ struct OpClsC10 {
   __device__ __forceinline__ void flush() {}
 };
 
+// dense packed bands (>= 2 wedges per counter word): no-return increments, closed by the
+// sweep -- (2,k) u16 b1 | u16 b2, classification pp | mm << 10 | pm << 20
+template <int MODE>
+struct OpPackedDense {
+  uint32_t rb;
+  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
+    if (MODE == kBicliques)
+      s_red_add(rb + (w << 2), 1u << (((w ^ sg) >> 27) & 16u));
+    else
+      s_red_add(rb + (w << 2), 1u << (10u * wedge_class(w, sg)));
+  }
+  __device__ __forceinline__ void flush() {}
+};
+
+// C(c, k) for the sweep (closed forms for k = 2, 3; c < 2^16 keeps them exact in 64 bits)
+__device__ __forceinline__ unsigned long long binom_k(unsigned long long c, uint32_t k) {
+  if (c < k) return 0ull;
+  if (k == 2u) return (c * (c - 1ull)) >> 1;
+  if (k == 3u) return c * (c - 1ull) * (c - 2ull) / 6ull;
+  return binom_dev(c, k);
+}
+
 // classification, three u32 words per end vertex, closed by the sweep; rb rebased by
 // lo_rank * 12
 struct OpClsC32 {
@@ -146,16 +171,22 @@ struct ExtSmem {
   unsigned long long* w;
 };
 
-// One anchor: bands from the top, record batches of T, inline closing (or the C32 sweep).
+// One anchor: bands from the top, record batches of T.  Packed layouts use one table
+// column per band when the band table exists (bounds from the table, or a galloping search
+// from the previous band's bound); a band holding >= 2 wedges per counter word (estimated
+// from its first batch) is counted with no-return increments and swept, others close
+// inline from the atomics' return values and are cleared with vector stores.
 template <int T, int MODE>
 __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uint32_t rb, uint32_t re,
                            unsigned long long (&acc)[12], uint32_t& ovf, unsigned long long& work) {
   const uint32_t deg = re - rb;
   const bool wide = MODE == kClassify ? deg > 1023u : deg > 65535u;
   const uint32_t wpv = wide ? (MODE == kClassify ? 3u : 2u) : 1u;  // words per end vertex
-  const uint32_t span = P.cap_words / wpv;
+  const bool cols = !wide && P.bnd != nullptr && P.t16 > 0u && P.t16 <= P.cap_words;
+  const uint32_t span = cols ? P.t16 : P.cap_words / wpv;
   const uint32_t nbands = (P.n - 1u - r) / span + 1u;  // bands 0..nbands-1 hold ranks > r
-  const bool single = deg <= (uint32_t)T;
+  const uint32_t nbatch = (deg + T - 1u) / (uint32_t)T;
+  const bool single = nbatch == 1u;
   const uint32_t base = sptr(S.cnt);
   uint32_t scan_buf = 0;
   uint32_t carry = 0;  // single batch: this record's upper bound for the next band
@@ -166,6 +197,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
     const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
     const uint32_t band_words = (uint32_t)(top - (long long)lo_rank) * wpv;
     unsigned long long band_w = 0;
+    int dense = -1;
     for (uint32_t b0 = rb; b0 < re; b0 += T) {
       const int nb = (int)min((uint32_t)T, re - b0);
       uint32_t ng = 0;
@@ -173,14 +205,23 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
       if ((int)threadIdx.x < nb) {
         const uint2 rr = P.rec[b0 + threadIdx.x];
         const uint32_t begin = rr.x & 0x7fffffffu;
-        uint32_t hi;
-        if (b == 0)
-          hi = __ldg(P.coff + rr.y + 1);
-        else if (single)
-          hi = carry;
-        else
-          hi = lower_bound_rank(P.adj, begin, __ldg(P.coff + rr.y + 1), top);
-        const uint32_t lo = lower_bound_rank(P.adj, begin, hi, bot);
+        const uint32_t bi = cols ? __ldg(P.brow + rr.y) : 0xffffffffu;
+        uint32_t hi, lo;
+        if (bi != 0xffffffffu) {
+          const uint32_t* row = P.bnd + (size_t)bi * P.nbands;
+          hi = __ldg(row + b);
+          lo = b + 1u < P.nbands ? __ldg(row + b + 1u) : 0u;
+        } else {
+          if (b == 0)
+            hi = __ldg(P.coff + rr.y + 1);
+          else if (single)
+            hi = carry;
+          else
+            hi = lower_bound_rank(P.adj, begin, __ldg(P.coff + rr.y + 1), top);
+          lo = single ? lower_bound_gallop(P.adj, begin, hi, bot) : lower_bound_rank(P.adj, begin, hi, bot);
+        }
+        lo = max(lo, begin);
+        hi = max(hi, lo);
         carry = lo;
         if (hi > lo) {
           ng = unit_count(lo, hi);
@@ -196,8 +237,12 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
       __syncthreads();
       work += myw;
       band_w += bw;
+      if (dense < 0) dense = (wide && MODE == kClassify) || (!wide && bw * nbatch >= 2ull * band_words);
       if (ngroups) {
-        if (MODE == kBicliques) {
+        if (dense && !wide) {
+          OpPackedDense<MODE> op{base - (lo_rank << 2)};
+          walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+        } else if (MODE == kBicliques) {
           OpBiclW16 x;
           if (!wide) {
             OpBiclW16 op;
@@ -235,19 +280,44 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
     if (band_w == 0ull) continue;
     uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
     const uint32_t nq = (band_words + 3u) / 4u;
-    if (MODE == kClassify && wide) {
-      // closing sweep over (pp, mm, pm) triples
-      for (uint32_t i = threadIdx.x; i < (band_words / 3u); i += T) {
-        const unsigned long long a = S.cnt[3u * i], bb = S.cnt[3u * i + 1u], d = S.cnt[3u * i + 2u];
-        part[0] += a * (a - (a > 0)) / 2;
-        part[1] += a * bb;
-        part[2] += bb * (bb - (bb > 0)) / 2;
-        part[3] += d * (d - (d > 0)) / 2;
-        part[4] += a * d;
-        part[5] += bb * d;
+    if (dense) {
+      if (MODE == kClassify && wide) {
+        // closing sweep over (pp, mm, pm) triples
+        for (uint32_t i = threadIdx.x; i < (band_words / 3u); i += T) {
+          const unsigned long long a = S.cnt[3u * i], bb = S.cnt[3u * i + 1u], d = S.cnt[3u * i + 2u];
+          part[0] += a * (a - (a > 0)) / 2;
+          part[1] += a * bb;
+          part[2] += bb * (bb - (bb > 0)) / 2;
+          part[3] += d * (d - (d > 0)) / 2;
+          part[4] += a * d;
+          part[5] += bb * d;
+        }
+      } else if (MODE == kClassify) {
+        for (uint32_t i = threadIdx.x; i < band_words; i += T) {
+          const uint32_t x = S.cnt[i];
+          if (x == 0u) continue;
+          const unsigned long long a = x & 1023u, bb = (x >> 10) & 1023u, d = x >> 20;
+          part[0] += a * (a - (a > 0)) / 2;
+          part[1] += a * bb;
+          part[2] += bb * (bb - (bb > 0)) / 2;
+          part[3] += d * (d - (d > 0)) / 2;
+          part[4] += a * d;
+          part[5] += bb * d;
+        }
+      } else {
+        const uint32_t k = P.k1 + 1u;
+        for (uint32_t i = threadIdx.x; i < band_words; i += T) {
+          const uint32_t x = S.cnt[i];
+          if (x == 0u) continue;
+          const unsigned long long v = binom_k(x & 0xffffu, k), w = binom_k(x >> 16, k);
+          if (v == ~0ull || w == ~0ull) ovf = 1u;
+          add128(acc[0], acc[1], v);
+          add128(acc[0], acc[1], w);
+        }
       }
       __syncthreads();
     }
+#pragma unroll 4
     for (uint32_t i = threadIdx.x; i < nq; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
   }
@@ -328,7 +398,7 @@ int ext_launch(Graph& g, const bbc_opts& opts, uint32_t k, unsigned long long* h
   BBC_CK(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, g.device));
   const int budget = std::min(g.max_smem, per_sm / MINB - 1024);
   const int avail = budget - (int)fa.sharedSizeBytes - (3 * T * 4 + 64);
-  const int cap_words = (avail / 48) * 12;  // a multiple of 12 (C32 triples, uint4 clearing)
+  const int cap_words = (avail / 16) * 4;  // as the count kernel: the band table columns fit
   const int smem_bytes = cap_words * 4 + 3 * T * 4 + 16;
   BBC_CK(cudaFuncSetAttribute(k_ext<T, MINB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
   const int blocks = opts.blocks > 0 ? opts.blocks : g.num_sms * MINB;
@@ -347,6 +417,10 @@ int ext_launch(Graph& g, const bbc_opts& opts, uint32_t k, unsigned long long* h
   P.aoff = g.aoff;
   P.awork = g.awork;
   P.order = g.order;
+  P.bnd = (opts.flags & 1024) ? nullptr : g.bnd;  // flags bit 10: searches only (tests)
+  P.brow = g.brow;
+  P.nbands = g.nbands;
+  P.t16 = g.t16;
   P.n = n;
   P.ntasks = n > (uint32_t)opts.part_index ? (n - (uint32_t)opts.part_index + part_count - 1) / part_count : 0u;
   P.part_index = (uint32_t)opts.part_index;
