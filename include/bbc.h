@@ -50,7 +50,12 @@ enum bbc_status {
   BBC_ERR_ARG = 4,      /* ValueError (bad sizes, options, sign not +-1)        */
   BBC_ERR_CUDA = 5,     /* BBCountError                                         */
   BBC_ERR_NCCL = 6,     /* BBCountError (reserved: collectives run host-side)   */
-  BBC_ERR_NOMEM = 7     /* BBCountError (device allocation failed)              */
+  BBC_ERR_NOMEM = 7,    /* BBCountError (device allocation failed)              */
+  BBC_ERR_PARSE = 8,    /* MalformedLineError; info = 1-based line               */
+  BBC_ERR_MISSING = 9,  /* MissingValueError; info = 1-based line of the edge    */
+  BBC_ERR_SIGNVAL = 10, /* InvalidSignValueError; info = 1-based line            */
+  BBC_ERR_UNSUPPORTED = 11 /* input outside the device loader's exact fast paths:
+                              use the host loader; info = 1-based line           */
 };
 
 enum bbc_algo {
@@ -123,6 +128,31 @@ int bbc_classify(bbc_graph* g, const bbc_opts* opts, uint64_t out[12], bbc_stats
  * out[0], out[1] = low / high 64 bits; BBC_ERR_ARG for k < 2 (InvalidKError);
  * BBC_ERR_OVERFLOW above 2^64-1 (CountOverflowError). */
 int bbc_count_2k(bbc_graph* g, int32_t k, const bbc_opts* opts, uint64_t out[2], bbc_stats* stats);
+
+/* device-side ingestion, replacing load_graph =
+ * parse_edge_list -> apply_sign_policy -> dedup_latest -> to_graph
+ * (pkg/src/bbcount/ingest.py:80-191) for ASCII edge-list text ('\n' line ends; tokens
+ * "u v [value] [timestamp]"; '%' / '#' comments).  Labels become dense ids per side in
+ * first-occurrence order; the deduplicated edges keep the pairs' first-occurrence order. */
+typedef struct {
+  int32_t kind;         /* 0 ExplicitSign, 1 RatingThreshold, 2 RandomBernoulli        */
+  int32_t at_or_above;  /* RatingThreshold.at_or_above_is_positive                    */
+  double threshold;     /* RatingThreshold.threshold                                  */
+  double p_positive;    /* RandomBernoulli.p_positive                                 */
+  uint64_t seed;        /* RandomBernoulli.seed & (2^64 - 1)                          */
+} bbc_sign_policy;
+
+typedef struct bbc_ingest bbc_ingest;
+
+/* counts = {n_u, n_v, m (deduplicated edges)}; errors BBC_ERR_PARSE / _MISSING /
+ * _SIGNVAL (first offending line, as the reference raises them) or _UNSUPPORTED. */
+int bbc_ingest_text(int device, const char* text, int64_t nbytes, const bbc_sign_policy* policy,
+                    int64_t counts[3], bbc_ingest** out);
+/* The m edges to host arrays (u:int32, v:int32, sign:int8 in {+1,-1}). */
+int bbc_ingest_edges(bbc_ingest* h, int32_t* u, int32_t* v, int8_t* sign);
+/* Build the counting graph straight from the ingested device arrays. */
+int bbc_ingest_graph(bbc_ingest* h, int32_t side_rule, bbc_graph** out);
+void bbc_ingest_destroy(bbc_ingest* h);
 
 /* Per-CTA admitted wedges of the last bbc_count (ScheduleReport.per_block_work). */
 int bbc_block_work(bbc_graph* g, uint64_t* out, int32_t n);

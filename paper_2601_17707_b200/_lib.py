@@ -31,7 +31,8 @@ FLAG_ROUNDS = 4096  # record per-kind round counters (round_counters())
 
 EXPORTED_SYMBOLS = (
     "bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work", "bbc_task_order",
-    "bbc_round_counters", "bbc_classify", "bbc_count_2k", "bbc_graph_info", "bbc_graph_stream", "bbc_graph_destroy", "bbc_device_count", "bbc_last_error",
+    "bbc_round_counters", "bbc_classify", "bbc_count_2k", "bbc_ingest_text", "bbc_ingest_edges",
+    "bbc_ingest_graph", "bbc_ingest_destroy", "bbc_graph_info", "bbc_graph_stream", "bbc_graph_destroy", "bbc_device_count", "bbc_last_error",
     "bbc_last_error_info",
 )
 
@@ -49,6 +50,13 @@ class Stats(ctypes.Structure):
                 ("tile_span", ctypes.c_int32), ("tasks", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("preprocess_ms", ctypes.c_float), ("count_ms", ctypes.c_float)]
 
+
+class SignPolicy(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("at_or_above", ctypes.c_int32), ("threshold", ctypes.c_double),
+                ("p_positive", ctypes.c_double), ("seed", ctypes.c_uint64)]
+
+
+ERR_PARSE, ERR_MISSING, ERR_SIGNVAL, ERR_UNSUPPORTED = 8, 9, 10, 11
 
 _lock = threading.Lock()
 _lib = None
@@ -72,6 +80,12 @@ def load() -> ctypes.CDLL:
         L.bbc_round_counters.argtypes = [P, U64P]
         L.bbc_classify.argtypes = [P, ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
         L.bbc_count_2k.argtypes = [P, I32, ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
+        L.bbc_ingest_text.argtypes = [ctypes.c_int, ctypes.c_char_p, I64, ctypes.POINTER(SignPolicy),
+                                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(P)]
+        L.bbc_ingest_edges.argtypes = [P, P, P, P]
+        L.bbc_ingest_graph.argtypes = [P, I32, ctypes.POINTER(P)]
+        L.bbc_ingest_destroy.argtypes = [P]
+        L.bbc_ingest_destroy.restype = None
         L.bbc_graph_info.argtypes = [P, ctypes.POINTER(ctypes.c_int64), I32]
         L.bbc_graph_stream.argtypes = [P]
         L.bbc_graph_stream.restype = P
@@ -82,7 +96,7 @@ def load() -> ctypes.CDLL:
         L.bbc_last_error_info.restype = ctypes.c_int64
         for name in ("bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work",
                      "bbc_task_order", "bbc_round_counters", "bbc_classify", "bbc_count_2k", "bbc_graph_info",
-                     "bbc_device_count"):
+                     "bbc_device_count", "bbc_ingest_text", "bbc_ingest_edges", "bbc_ingest_graph"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
         return L
@@ -249,3 +263,49 @@ class DeviceGraph:
             self.close()
         except Exception:
             pass
+
+
+class Ingested:
+    """Owning handle of a device-side ingestion (bbc_ingest*): the deduplicated signed edges
+    with dense first-occurrence ids, resident on the device."""
+
+    def __init__(self, handle: int, device: int, n_u: int, n_v: int, m: int):
+        self._h = ctypes.c_void_p(handle)
+        self.device, self.n_u, self.n_v, self.m = device, n_u, n_v, m
+
+    def edges(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        u = np.empty(max(self.m, 1), dtype=np.int32)
+        v = np.empty(max(self.m, 1), dtype=np.int32)
+        s = np.empty(max(self.m, 1), dtype=np.int8)
+        rc = load().bbc_ingest_edges(self._h, u.ctypes.data, v.ctypes.data, s.ctypes.data)
+        if rc:
+            _raise(rc)
+        return u[:self.m], v[:self.m], s[:self.m]
+
+    def device_graph(self, side_rule: int = SIDE_CHEAPER) -> "DeviceGraph":
+        h = ctypes.c_void_p()
+        rc = load().bbc_ingest_graph(self._h, side_rule, ctypes.byref(h))
+        if rc:
+            _raise(rc)
+        return DeviceGraph(h.value, self.device)
+
+    def close(self) -> None:
+        if self._h is not None and self._h.value:
+            load().bbc_ingest_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ingest_text(data: bytes, policy: SignPolicy, device: int = 0) -> tuple[int, "Ingested | None", int]:
+    """(status, handle or None, 1-based line of the first problem) of bbc_ingest_text."""
+    counts = (ctypes.c_int64 * 3)()
+    h = ctypes.c_void_p()
+    rc = load().bbc_ingest_text(device, data, len(data), ctypes.byref(policy), counts, ctypes.byref(h))
+    if rc:
+        return rc, None, int(load().bbc_last_error_info())
+    return 0, Ingested(h.value, device, int(counts[0]), int(counts[1]), int(counts[2])), 0

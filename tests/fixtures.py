@@ -151,3 +151,50 @@ CORPORA = {
     "skewed_sign_30": (2929, 80, 30, 30, 0.3, 0.85),
     "tall_thin": (4141, 60, 60, 8, 0.4, 0.5),
 }
+
+
+# ---- edge-list texts for the loaders (device ingestion) --------
+
+def ingest_text(seed: int, n_lines: int, n_u: int, n_v: int, kind: str = "explicit", dup: float = 0.2,
+                ts: float = 0.5) -> str:
+    """Deterministic edge-list text in the reference's input format (ingest.py:80-115):
+    comment and blank lines, string labels, repeated (u, v) pairs with and without
+    timestamps, values as signs ("1", "-1", "0", "1.0", "+1", "-0") or ratings."""
+    rng = random.Random(seed)
+    lines = ["% generated edge list", "# second comment", ""]
+    pairs: list[tuple[str, str]] = []
+    for _ in range(n_lines):
+        r = rng.random()
+        if r < 0.02:
+            lines.append(rng.choice(["", "   ", "% note", "#x y z", "\t"]))
+            continue
+        if pairs and r < 0.02 + dup:
+            a, b = rng.choice(pairs)
+        else:
+            a = rng.choice(["u", "user", "U_", ""]) + str(rng.randrange(n_u))
+            b = rng.choice(["v", "item", "V-", ""]) + str(rng.randrange(n_v))
+            pairs.append((a, b))
+        if kind == "explicit":
+            val = rng.choice(["1", "-1", "0", "1.0", "+1", "-0", "1e0", "-1.000"])
+        elif kind == "rating":
+            val = rng.choice(["1", "2", "3", "3.5", "4", "5", "4.25", "2.5e0", "10"])
+        else:
+            val = rng.choice(["", "1", "7"])
+        sep = rng.choice([" ", "\t", "  ", " \t "])
+        parts = [a, b] + ([val] if val else [])
+        if val and rng.random() < ts:
+            parts.append(str(rng.randrange(-5, 50)))
+        lines.append(rng.choice(["", " ", "\t"]) + sep.join(parts) + rng.choice(["", " ", "\r", "\t"]))
+    return "\n".join(lines) + rng.choice(["", "\n"])
+
+
+INGEST_CASES = {
+    # name: (seed, n_lines, n_u, n_v, kind, policy)  policy: ("explicit",) | ("rating", t, at_or_above)
+    #                                                        | ("bernoulli", p, seed)
+    "explicit_small": (11, 200, 20, 15, "explicit", ("explicit",)),
+    "explicit_dups": (12, 3000, 60, 40, "explicit", ("explicit",)),
+    "rating_at_or_above": (13, 2000, 50, 80, "rating", ("rating", 3.5, True)),
+    "rating_strict": (14, 2000, 50, 80, "rating", ("rating", 4.0, False)),
+    "bernoulli": (15, 2500, 70, 70, "bare", ("bernoulli", 0.7, 20260810)),
+    "bernoulli_big_seed": (16, 500, 30, 30, "bare", ("bernoulli", 0.35, 2**64 + 12345)),
+}

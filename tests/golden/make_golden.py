@@ -6,6 +6,7 @@ absent on the GPU box, which only reads the committed JSON):
     python tests/golden/make_golden.py            # fixtures, corpora, config 1, scaled configs
     python tests/golden/make_golden.py --full 2   # config 2 at full size (long: ~30 min)
     python tests/golden/make_golden.py --ext      # classification + (2,k) vectors (8(f))
+    python tests/golden/make_golden.py --ingest   # loader vectors (8(f) rank 3)
 
 Every count here comes from the reference's own engines (pkg/src/bbcount):
   balanced  = count_balanced_parallel(g, workers)        (buckets.py:213-246)
@@ -203,6 +204,25 @@ def extensions(out: dict) -> None:
         print(f"config {key} extensions in {time.time() - t0:.1f}s: {rec['classes']} {rec['b2k']}", flush=True)
 
 
+def ingest(out: dict) -> None:
+    """Loader vectors: the reference's load_graph (ingest.py:185-191)
+    on deterministic texts from tests/fixtures.ingest_text, recorded as sorted-edge digests."""
+    def policy(p):
+        if p[0] == "explicit":
+            return bbcount.ExplicitSign()
+        if p[0] == "rating":
+            return bbcount.RatingThreshold(p[1], p[2])
+        return bbcount.RandomBernoulli(p[1], p[2])
+
+    rec = {}
+    for name, (seed, n, nu, nv, kind, pol) in fixtures.INGEST_CASES.items():
+        text = fixtures.ingest_text(seed, n, nu, nv, kind)
+        g = bbcount.load_graph(text, policy(pol))
+        rec[name] = {"n_u": g.u_count, "n_v": g.v_count, "m": g.edge_count, "digest": ref_digest(g),
+                     "text_len": len(text)}
+    out["ingest"] = rec
+
+
 def main() -> None:
     path = HERE / "golden.json"
     out = json.loads(path.read_text()) if path.exists() else {}
@@ -210,7 +230,9 @@ def main() -> None:
     out.setdefault("corpora", {})
     out.setdefault("configs", {})
     out["generator"] = "tests/golden/make_golden.py (reference bbcount 0.1.0 at /root/reference/pkg/src)"
-    if "--ext" in sys.argv:
+    if "--ingest" in sys.argv:
+        ingest(out)
+    elif "--ext" in sys.argv:
         extensions(out)
     elif "--full" in sys.argv:
         cfg_id = int(sys.argv[sys.argv.index("--full") + 1])

@@ -275,3 +275,26 @@ def test_synth_generator_deterministic_and_distinct(native_built):
     key = a[0].astype(np.int64) * cfg.n_v + a[1]
     assert len(np.unique(key)) == cfg.m
     assert (a[0] < cfg.n_u).all() and (a[1] < cfg.n_v).all() and set(np.unique(a[2])) <= {-1, 1}
+
+
+def _policy(p):
+    if p[0] == "explicit":
+        return ExplicitSign()
+    if p[0] == "rating":
+        return RatingThreshold(p[1], p[2])
+    return RandomBernoulli(p[1], p[2])
+
+
+def test_host_loader_matches_reference_ingest_vectors(golden):
+    """The host loader against the reference's load_graph on the same texts
+    (tests/golden/make_golden.py --ingest)."""
+    from paper_2601_17707_b200 import synth
+
+    for name, (seed, n, nu, nv, kind, pol) in fixtures.INGEST_CASES.items():
+        text = fixtures.ingest_text(seed, n, nu, nv, kind)
+        rec = golden["ingest"][name]
+        assert len(text) == rec["text_len"], name
+        g = load_graph(text, _policy(pol))
+        u, v, s = g.edge_arrays()
+        assert (g.u_count, g.v_count, g.edge_count) == (rec["n_u"], rec["n_v"], rec["m"]), name
+        assert synth.edge_digest(u, v, s) == rec["digest"], name
