@@ -35,10 +35,14 @@ namespace {
 
 constexpr int kT = 256;
 
+// temporaries are stream-ordered allocations from the device's (cached) default pool, so
+// repeated ingestions do not pay cudaMalloc / cudaFree round trips
+thread_local cudaStream_t t_stream = nullptr;
+
 struct Buf {
   void* p = nullptr;
   ~Buf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, t_stream);
   }
   template <typename X>
   X* as() {
@@ -46,10 +50,10 @@ struct Buf {
   }
 };
 
-#define ING_ALLOC(buf, bytes)                                              \
-  do {                                                                     \
-    cudaError_t _e = cudaMalloc(&(buf).p, (bytes) ? (size_t)(bytes) : 16); \
-    if (_e != cudaSuccess) return cuda_fail(_e, "cudaMalloc (ingest)");    \
+#define ING_ALLOC(buf, bytes)                                                             \
+  do {                                                                                    \
+    cudaError_t _e = cudaMallocAsync(&(buf).p, (bytes) ? (size_t)(bytes) : 16, t_stream); \
+    if (_e != cudaSuccess) return cuda_fail(_e, "cudaMallocAsync (ingest)");             \
   } while (0)
 
 inline int grid(int64_t n) {
@@ -489,8 +493,20 @@ int ingest_text(int device, const char* text, int64_t nbytes, const bbc_sign_pol
   BBC_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   struct StreamGuard {
     cudaStream_t s;
-    ~StreamGuard() { cudaStreamDestroy(s); }
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+      t_stream = nullptr;
+    }
   } guard{st};
+  t_stream = st;
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   out.device = device;
   if (nbytes <= 0) return BBC_OK;
   Buf t, nl, nnl, temp, status, lines, scal, eline, ne;
