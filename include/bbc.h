@@ -78,7 +78,19 @@ typedef struct {
   int32_t partial_max;
   int32_t part_index;   /* start-vertex partition [part_index of part_count]        */
   int32_t part_count;   /* 0 or 1 = whole graph                                     */
-  int32_t flags;        /* bit 0: general banded path only (testing)                */
+  int32_t flags;        /* 0 in production; testing / measurement switches:         */
+                        /*  bit 0  general banded path only                           */
+                        /*  bit 1  no cold key-hash rounds                            */
+                        /*  bit 2  skip the hub band, bit 3 skip the cold range       */
+                        /*         (timing only: the counts are then partial)         */
+                        /*  bit 6  hub / cold range in two launches (experimental)    */
+                        /*  bit 7  cold range in counter tiles only                   */
+                        /*  bit 8  tiny repeat queue (exercises overflow + narrowing) */
+                        /*  bit 9  force cold bitmap rounds                           */
+                        /*  bit 10 band bounds by search (ignore the band table)      */
+                        /*  bit 11 closing sweep for every tile round                 */
+                        /*  bit 12 record round counters (bbc_round_counters)         */
+                        /*  bit 13 force cold key-hash rounds                         */
 } bbc_opts;
 
 typedef struct {
