@@ -380,7 +380,6 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   const uint32_t ncols = min(P.nbands, (P.n - 1u - r) / t16 + 1u);  // columns holding ranks > r
   const int nb = (int)(re - rb);
   const bool mine = (int)threadIdx.x < nb;
-  uint32_t scan_buf = 0;  // alternates the scan's total buffers
   uint32_t recx = 0u, lend = 0u;
   const uint32_t* row = nullptr;
   if (mine) {
@@ -408,28 +407,58 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   const uint32_t cn = (P.phase == 1 || !(P.debug & 4)) ? 0u : col(ncols, c1);
   // sub-slices [lo, hi) (positions of two table columns) -> S arrays, block scan;
   // returns total groups, bw = total wedges
+  // One barrier per round set-up: each thread publishes its record's sub-slice, then EVERY
+  // warp scans all (<= T) records itself (T / 32 per lane) and writes the same prefix
+  // values to S.pfx -- a benign race, and a warp only reads pfx after writing it.  A round
+  // without chunks adds a barrier so that no warp overwrites S.lo / S.hi while another
+  // still scans them.
   auto setup = [&](uint32_t hi, uint32_t lo, unsigned long long& bw) -> uint32_t {
-    uint32_t ng = 0;
-    unsigned long long myw = 0;
     if (mine) {
       lo = max(lo, recx & 0x7fffffffu);
       hi = max(hi, lo);
-      if (hi > lo) {
-        ng = unit_count(lo, hi);
-        myw = hi - lo;
-      }
       S.lo[threadIdx.x] = lo | (recx & 0x80000000u);
       S.hi[threadIdx.x] = hi;
     }
-    uint32_t ngroups;
-    const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w, scan_buf++);
-    if (mine) S.pfx[threadIdx.x] = ex;
+    __syncthreads();
+    constexpr int R = T / 32;
+    const int lane = threadIdx.x & 31;
+    uint32_t ng[R], run = 0;
+    unsigned long long wsum = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int k = lane * R + i;
+      ng[i] = 0u;
+      if (k < nb) {
+        const uint32_t a = S.lo[k] & 0x7fffffffu, b = S.hi[k];
+        ng[i] = unit_count(a, b) & (b > a ? 0xffffffffu : 0u);
+        wsum += b - a;
+      }
+      run += ng[i];
+    }
+    uint32_t incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
+    uint32_t ex = incl - run;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int k = lane * R + i;
+      if (k < nb) S.pfx[k] = ex;
+      ex += ng[i];
+    }
+    const uint32_t ngroups = __shfl_sync(kFull, incl, 31);
+    bw = wsum;
+    __syncwarp();
     if ((P.debug & 4096) && threadIdx.x == 0) {
       atomicAdd(P.acc + 8, (unsigned long long)ngroups);
       atomicAdd(P.acc + 9, bw);
       atomicAdd(P.acc + 10, 1ull);
     }
-    __syncthreads();
+    if (ngroups == 0u) __syncthreads();
     return ngroups;
   };
   // one tile round over band columns [ca, ca + cols)
@@ -622,6 +651,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       }
       if (bw > target && cols > 1u) {  // too many wedges for the hash: narrower, no walk
         cols = max(1u, min(cols / 2u, (uint32_t)((unsigned long long)cols * target / bw)));
+        __syncthreads();  // every warp is done with this set-up's record arrays
         continue;
       }
       if (bw > target) {  // a single column denser than the hash: one counter-tile round
