@@ -7,9 +7,8 @@
 
 namespace bbc {
 
-int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st);
+int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st, int32_t k = 2);
 int classify_graph(Graph& g, const bbc_opts* o, uint64_t out[12], bbc_stats* st);
-int count_2k_graph(Graph& g, int32_t k, const bbc_opts* o, uint64_t out[2], bbc_stats* st);
 
 namespace {
 thread_local std::string t_err;
@@ -53,7 +52,18 @@ int bbc_count_2k(bbc_graph* h, int32_t k, const bbc_opts* opts, uint64_t out[2],
     bbc::set_error("graph handle and out must not be null");
     return BBC_ERR_ARG;
   }
-  return bbc::count_2k_graph(h->g, k, opts, out, stats);
+  // the count kernel with C(., k) closings (hub tiles, cold bitmap / hash rounds)
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if (k != 2) return bbc::count_graph(h->g, opts, out, stats, k);
+  // k = 2: the balanced butterfly count (its high word in out[1])
+  bbc_stats st{};
+  uint64_t o2[2] = {0, 0};
+  int rc = bbc::count_graph(h->g, opts, o2, &st, 2);
+  if (stats) *stats = st;
+  out[0] = o2[0];
+  out[1] = st.balanced_hi;
+  if (rc == BBC_ERR_OVERFLOW && st.balanced_hi == 0) rc = BBC_OK;  // only unbalanced overflowed
+  return rc;
 }
 
 int bbc_block_work(bbc_graph* h, uint64_t* out, int32_t n) {

@@ -72,6 +72,7 @@ struct Params {
   uint32_t sweep_min;  // tile rounds with >= sweep_min wedges per counter word close by sweep
   uint32_t fast_max;  // largest degree on the fast path (same for every launch of a count)
   int debug;        // flags bits 2 / 3: skip band 0 / skip the cold range (timing only)
+  uint32_t k;       // (2,k)-bicliques (k > 2: the KG kernel); 2 = balanced / unbalanced
   int dynamic;
   unsigned long long* acc;
   unsigned int* queue;
@@ -110,36 +111,60 @@ struct OpTileDense32 {
 // positive count to balanced and the old negative count to unbalanced, a - wedge the
 // reverse); 32-bit partial sums per pair (8 x 65535 < 2^32), flushed to 64 bits.  With
 // KEEP the touched word of each slot is kept (single-iteration rounds zero from it).
-template <int W, bool KEEP>
+template <int W, bool KEEP, bool KG = false>
 struct OpTileClose {
   uint32_t rb;
   unsigned long long *tb, *tu;
+  uint32_t k = 2;  // KG: (2,k)-bicliques, a wedge on a bucket holding c adds C(c, k-1)
   uint32_t b32 = 0, u32 = 0;
   uint32_t touched[8];
+  __device__ __forceinline__ void add(uint32_t c, uint32_t other) {
+    if (KG) {
+      if (c >= k - 1u) add_k(*tb, *tu, binom_k(c, k - 1u));
+    } else {
+      b32 += c;
+      u32 += other;
+    }
+  }
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int j) {
     const uint32_t v = w ^ sg;
     if (W == 8) {
       const uint32_t sh = ((w & 1u) << 4) | ((v >> 28) & 8u);
       const uint32_t a = rb + ((w << 1) & 0xfffffffcu);
       const uint32_t old = s_atom_add(a, 1u << sh);
-      b32 += (old >> sh) & 0xffu;
-      u32 += (old >> (sh ^ 8u)) & 0xffu;
+      add((old >> sh) & 0xffu, (old >> (sh ^ 8u)) & 0xffu);
       if (KEEP) touched[j] = a;
     } else {
       const uint32_t sh = (v >> 27) & 16u;
       const uint32_t a = rb + ((w << 2) & 0xfffffffcu);
       const uint32_t old = s_atom_add(a, 1u << sh);
-      b32 += (old >> sh) & 0xffffu;
-      u32 += (old >> (sh ^ 16u)) & 0xffffu;
+      add((old >> sh) & 0xffffu, (old >> (sh ^ 16u)) & 0xffffu);
       if (KEEP) touched[j] = a;
     }
   }
   __device__ __forceinline__ void flush() {
-    *tb += b32;
-    *tu += u32;
-    b32 = u32 = 0u;
+    if (!KG) {
+      *tb += b32;
+      *tu += u32;
+      b32 = u32 = 0u;
+    }
   }
 };
+
+// closing of one end vertex with p symmetric and q asymmetric wedges: k = 2 adds
+// C(p,2)+C(q,2) to balanced (tb) and p*q to unbalanced (tu); KG adds C(p,k)+C(q,k) to the
+// 128-bit (tb, tu)
+template <bool KG>
+__device__ __forceinline__ void close_pq(unsigned long long p, unsigned long long q, uint32_t k,
+                                         unsigned long long& tb, unsigned long long& tu) {
+  if (KG) {
+    add_k(tb, tu, binom_k(p, k));
+    add_k(tb, tu, binom_k(q, k));
+  } else {
+    tb += ((p * (p - (p > 0))) >> 1) + ((q * (q - (q > 0))) >> 1);
+    tu += p * q;
+  }
+}
 
 // ---- very wide cold ranges: key hash + repeat queue ------------------------------------
 // When the cold range spans so many ranks that bitmap rounds would hold only a few hundred
@@ -222,15 +247,28 @@ __device__ __forceinline__ uint32_t rep_insert(uint32_t* keys, uint32_t K, uint3
 __device__ __forceinline__ unsigned long long c2(unsigned long long x) { return x * (x - (x > 0)) >> 1; }
 
 // closing sweep over `words` counter words of layout W
-template <int T, int W>
-__device__ __forceinline__ void sweep(uint32_t* cnt, uint32_t words, unsigned long long& tb, unsigned long long& tu) {
+template <int T, int W, bool KG = false>
+__device__ __forceinline__ void sweep(uint32_t* cnt, uint32_t words, unsigned long long& tb, unsigned long long& tu,
+                                      uint32_t k = 2) {
   uint4* c4 = reinterpret_cast<uint4*>(cnt);
   const uint32_t nq = (words + 3) >> 2;
   for (uint32_t i = threadIdx.x; i < nq; i += T) {
     const uint4 x = c4[i];
     if ((x.x | x.y | x.z | x.w) == 0u) continue;
     const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-    if (W == 8) {
+    if (KG) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (W == 8) {
+          close_pq<true>(xs[j] & 0xffu, (xs[j] >> 8) & 0xffu, k, tb, tu);
+          close_pq<true>((xs[j] >> 16) & 0xffu, xs[j] >> 24, k, tb, tu);
+        } else if (W == 16) {
+          close_pq<true>(xs[j] & 0xffffu, xs[j] >> 16, k, tb, tu);
+        } else {
+          add_k(tb, tu, binom_k(xs[j], k));
+        }
+      }
+    } else if (W == 8) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint32_t p0 = xs[j] & 0xffu, q0 = (xs[j] >> 8) & 0xffu, p1 = (xs[j] >> 16) & 0xffu, q1 = xs[j] >> 24;
@@ -268,7 +306,7 @@ struct Smem {
 };
 
 // General path: any degree (records in batches of T), table or binary search, layout W.
-template <int T, int W>
+template <int T, int W, bool KG>
 __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint32_t rb, uint32_t re,
                                unsigned long long& tb, unsigned long long& tu, unsigned long long& work) {
   const uint32_t span = W == 8 ? P.span8 : (W == 16 ? P.span16 : P.span32);
@@ -339,7 +377,7 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
             walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
           }
         } else {
-          OpTileClose<W == 32 ? 16 : W, false> op{base, &tb, &tu};
+          OpTileClose<W == 32 ? 16 : W, false, KG> op{base, &tb, &tu, P.k};
           walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
         }
       }
@@ -347,7 +385,7 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
     }
     if (band_w > 0) {
       if (mode == kDense) {
-        sweep<T, W>(S.cnt, band_words, tb, tu);
+        sweep<T, W, KG>(S.cnt, band_words, tb, tu, P.k);
       } else {
         uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
 #pragma unroll 4
@@ -368,7 +406,7 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
 // Phase 0 runs both in one launch.  Tile rounds with <= 2 groups per thread close inline
 // and zero from registers; larger ones use no-return increments and the closing sweep.
 // Records stay in registers across rounds.
-template <int T, int W>
+template <int T, int W, bool KG>
 __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, uint32_t rb, uint32_t re,
                                     unsigned long long w_a, unsigned long long& tb, unsigned long long& tu,
                                     unsigned long long& work) {
@@ -474,7 +512,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     if (ngroups <= (uint32_t)T) {
       // at most one chunk per thread: close inline and zero the touched words
       // from registers (no second pass over the tile or the adjacency)
-      OpTileClose<W, true> op{base, &tb, &tu};
+      OpTileClose<W, true, KG> op{base, &tb, &tu, P.k};
 #pragma unroll
       for (int j = 0; j < 8; ++j) op.touched[j] = 0xffffffffu;
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
@@ -485,7 +523,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     } else if (bw < (unsigned long long)P.sweep_min * band_words && !(P.debug & 2048)) {
       // medium rounds: inline closing, then the tile is cleared with vector stores (a
       // closing sweep costs ~9 instructions per counter word, inline closing ~4 per wedge)
-      OpTileClose<W, false> op{base, &tb, &tu};
+      OpTileClose<W, false, KG> op{base, &tb, &tu, P.k};
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
       uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
@@ -495,7 +533,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       OpTileDense<W> op{base};
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
       __syncthreads();
-      sweep<T, W>(S.cnt, band_words, tb, tu);
+      sweep<T, W, KG>(S.cnt, band_words, tb, tu, P.k);
     }
     // no trailing barrier: every caller's next tile use comes after a setup (two barriers)
     // or after the end of the anchor (one barrier)
@@ -584,9 +622,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
           if (e == 0u) continue;
           const uint32_t h = e & 0x3fffffffu, neg = (e >> 30) & 1u;
           const uint32_t v = vals[h];
-          const unsigned long long pc = (v & 0xffffu) + (neg ^ 1u), qc = (v >> 16) + neg;
-          tb += ((pc * (pc - 1ull)) >> 1) + ((qc * (qc - 1ull)) >> 1);
-          tu += pc * qc;
+          close_pq<KG>((v & 0xffffu) + (neg ^ 1u), (v >> 16) + neg, P.k, tb, tu);
           keys[h] = 0u;
           vals[h] = 0u;
           queue[i] = 0u;
@@ -682,9 +718,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
           const uint32_t v = atomicExch(&cnts[e & 0x3fffffffu], 0u);
           if (v == 0u) continue;
           const unsigned long long neg = (e >> 30) & 1u;
-          const unsigned long long pc = (v & 0xffffu) + (neg ^ 1ull), qc = (v >> 16) + neg;
-          tb += ((pc * (pc - 1ull)) >> 1) + ((qc * (qc - 1ull)) >> 1);
-          tu += pc * qc;
+          close_pq<KG>((v & 0xffffu) + (neg ^ 1ull), (v >> 16) + neg, P.k, tb, tu);
         }
       } else if (ovf) {
         uint4* q4 = reinterpret_cast<uint4*>(queue);
@@ -736,7 +770,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   tiles();
 }
 
-template <int T, int MINB>
+template <int T, int MINB, bool KG>
 __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
   constexpr int kWarps = T / 32;
   extern __shared__ uint4 smem4[];
@@ -784,15 +818,15 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
       continue;
     }
     if (fast && deg <= 255u)
-      process_anchor_fast<T, 8>(P, S, r, rb, re, w_a, tb, tu, work);
+      process_anchor_fast<T, 8, KG>(P, S, r, rb, re, w_a, tb, tu, work);
     else if (fast)
-      process_anchor_fast<T, 16>(P, S, r, rb, re, w_a, tb, tu, work);
+      process_anchor_fast<T, 16, KG>(P, S, r, rb, re, w_a, tb, tu, work);
     else if (deg <= 255u)
-      process_anchor<T, 8>(P, S, r, rb, re, tb, tu, work);
+      process_anchor<T, 8, KG>(P, S, r, rb, re, tb, tu, work);
     else if (deg <= 65535u)
-      process_anchor<T, 16>(P, S, r, rb, re, tb, tu, work);
+      process_anchor<T, 16, KG>(P, S, r, rb, re, tb, tu, work);
     else
-      process_anchor<T, 32>(P, S, r, rb, re, tb, tu, work);
+      process_anchor<T, 32, KG>(P, S, r, rb, re, tb, tu, work);
     add128(bal_lo, bal_hi, tb);
     add128(unb_lo, unb_hi, tu);
     __syncthreads();  // publish the claimed task
@@ -836,10 +870,10 @@ struct Launch {
 
 // T threads per CTA, MINB CTAs per SM: shared memory is split evenly between the CTAs of
 // an SM (1 KB per CTA is reserved by the driver) and registers are capped accordingly.
-template <int T, int MINB>
+template <int T, int MINB, bool KG = false>
 int configure_t(Graph& g, Launch& L) {
   cudaFuncAttributes fa;
-  BBC_CK(cudaFuncGetAttributes(&fa, k_count<T, MINB>));
+  BBC_CK(cudaFuncGetAttributes(&fa, k_count<T, MINB, KG>));
   int per_sm = 0;
   BBC_CK(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, g.device));
   int budget = std::min(g.max_smem, per_sm / MINB - 1024);
@@ -848,29 +882,17 @@ int configure_t(Graph& g, Launch& L) {
   L.blocks_per_sm = MINB;
   L.cap_words = (avail / 16) * 4;
   L.smem_bytes = L.cap_words * 4 + 3 * T * 4 + 16;
-  L.kernel = k_count<T, MINB>;
-  BBC_CK(cudaFuncSetAttribute(k_count<T, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes));
+  L.kernel = k_count<T, MINB, KG>;
+  BBC_CK(cudaFuncSetAttribute(k_count<T, MINB, KG>, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes));
   return BBC_OK;
 }
 
-// single-launch configuration (all phases): BBC_THREADS, default 128 x 8 per SM
+// single-launch configuration (all phases): 128 x 8 per SM, or 256 x 4 (env BBC_THREADS=256,
+// an experiment).  Measured on config 2 and removed: 128 x {4, 6, 10, 12} (19.6 / 16.0 /
+// 17.7 / 20.0 ms vs 15.4 ms at the time) and 512 x 2 / 1024 x 1.
 int configure(Graph& g, Launch& L) {
-  switch (g.threads) {
-    case 256:
-      return configure_t<256, 4>(g, L);
-    case 512:
-      return configure_t<512, 2>(g, L);
-    case 1024:
-      return configure_t<1024, 1>(g, L);
-    default:
-      // 128-thread CTAs: 8 per SM (default) or, for experiments (env BBC_MINB), 10 / 12
-      // with fewer registers and smaller tiles, or 4 / 6 with larger tiles
-      if (g.minb == 12) return configure_t<128, 12>(g, L);
-      if (g.minb == 10) return configure_t<128, 10>(g, L);
-      if (g.minb == 6) return configure_t<128, 6>(g, L);
-      if (g.minb == 4) return configure_t<128, 4>(g, L);
-      return configure_t<128, 8>(g, L);
-  }
+  if (g.threads == 256) return configure_t<256, 4>(g, L);
+  return configure_t<128, 8>(g, L);
 }
 
 // two-phase configuration: hub band with 128 x 8, cold range with 256 x 2 (big hash)
@@ -888,7 +910,9 @@ int count_span16(Graph& g) {
   return L.cap_words - 8;
 }
 
-int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
+// k = 2: balanced / unbalanced butterflies; k > 2: balanced (2,k)-bicliques (out[0] = the
+// count, out[1] = 0) with the same rounds and C(., k) closings (the KG kernel)
+int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st, int32_t k) {
   bbc_opts opts{};
   if (o) opts = *o;
   if (opts.algo != BBC_ALGO_GBBC && opts.algo != BBC_ALGO_GBBCPP) {
@@ -904,16 +928,21 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     set_error("part_index must lie in [0, part_count)");
     return BBC_ERR_ARG;
   }
+  if (k < 2) {
+    set_error("k must be >= 2, got " + std::to_string(k));
+    return BBC_ERR_ARG;
+  }
+  const bool kg = k > 2;
   BBC_CK(cudaSetDevice(g.device));
   Launch L, Lc;
-  int rc = configure(g, L);
+  int rc = kg ? configure_t<128, 8, true>(g, L) : configure(g, L);
   if (rc) return rc;
   bool use_table = g.bnd != nullptr && !(opts.flags & 1024);  // 1024: binary search (tests)
   const bool tile_override = opts.tile_span > 0 && (uint32_t)opts.tile_span < 2u * ((uint32_t)L.cap_words - 8u);
   if (tile_override) use_table = false;
   // flags bit 6 (experimental, measured slower on config 2): hub band and cold range in
   // two launches with different CTA shapes
-  const bool two_phase = use_table && (opts.flags & 64) && (opts.flags & 1) == 0;
+  const bool two_phase = !kg && use_table && (opts.flags & 64) && (opts.flags & 1) == 0;
   if (two_phase) {
     rc = configure_cold(g, Lc);
     if (rc) return rc;
@@ -990,6 +1019,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     P.sweep_min = tune.sweep_min;
     P.debug = opts.flags;
     P.dynamic = opts.algo == BBC_ALGO_GBBCPP;
+    P.k = (uint32_t)k;
     P.acc = g.acc;
     P.queue = g.queue + (phase == 2 ? 1 : 0);
     P.block_work = g.block_work;
@@ -1017,6 +1047,13 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
   float ms = 0.f;
   cudaEventElapsedTime(&ms, g.ev0, g.ev1);
   for (int i = 0; i < 8; ++i) g.rounds[i] = h_acc[4 + i];
+  if (kg) {
+    // per-thread (tb, tu) were the low / high words of one 128-bit sum: total =
+    // bal + unb * 2^64 (as 128-bit values); the low 64 bits and whether it overflowed
+    const bool ovf = h_acc[1] != 0ull || h_acc[2] != 0ull || h_acc[3] != 0ull;
+    h_acc[1] = ovf ? 1ull : 0ull;
+    h_acc[2] = h_acc[3] = 0ull;
+  }
   out[0] = h_acc[0];
   out[1] = h_acc[2];
   if (st) {
@@ -1040,7 +1077,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
     st->count_ms = ms;
   }
   if (h_acc[1] || h_acc[3]) {
-    set_error("balanced/unbalanced count exceeded 64-bit range");
+    set_error(kg ? "balanced (2,k) count exceeded 64-bit range" : "balanced/unbalanced count exceeded 64-bit range");
     return BBC_ERR_OVERFLOW;
   }
   return BBC_OK;

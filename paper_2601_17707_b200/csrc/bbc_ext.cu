@@ -1,28 +1,23 @@
-// SURVEY.md 8(f) kernels on the same device CSR as the count kernel:
-//
-//   * six-way butterfly classification -- reference oracle.classify_butterflies
-//     (pkg/src/bbcount/oracle.py:172-197, ButterflyClassCounts :31-64).  Anchors are U
-//     vertices, centres V (the classes are not side-symmetric, oracle.py:176-178), so the
-//     graph must be built with BBC_SIDE_U.  For every anchor pair (u, w) the wedges
-//     through the common centres c split into pp (both edges +), mm (both -) and pm
-//     (signs differ); the classes are C(pp,2), pp*mm, C(mm,2), C(pm,2), pp*pm, mm*pm.
-//   * balanced (2,k)-bicliques, k >= 2 -- reference count_balanced_2k_serial
-//     (pkg/src/bbcount/buckets.py:64-154): per pair C(b1,k) + C(b2,k) with b1 / b2 the
-//     symmetric / asymmetric wedge counts (math.comb at :146), the size-2 side = the
-//     graph's anchor side; a total above 2^64-1 is CountOverflowError.
+// SURVEY.md 8(f) row 1 on the same device CSR as the count kernel: six-way butterfly
+// classification -- reference oracle.classify_butterflies (pkg/src/bbcount/oracle.py:
+// 172-197, ButterflyClassCounts :31-64).  Anchors are U vertices, centres V (the classes
+// are not side-symmetric, oracle.py:176-178), so the graph must be built with BBC_SIDE_U.
+// For every anchor pair (u, w) the wedges through the common centres c split into pp (both
+// edges +), mm (both -) and pm (signs differ); the classes are C(pp,2), pp*mm, C(mm,2),
+// C(pm,2), pp*pm, mm*pm.  (Row 2, (2,k)-bicliques, runs in the count kernel itself with
+// C(., k) closings: bbc_count.cu.)
 //
 // Structure (one CTA per anchor, persistent CTAs over the G-BBC++ queue or static
-// round-robin): the anchor's end-vertex ranks are cut into bands of S ranks from the top;
-// per band and per batch of <= T records, each record's admitted sub-slice is found by
-// binary search (the next band's upper bound is carried), a block scan lays the int4
-// groups out and the pair walker (bbc_walk.cuh) increments a shared-memory counter per end
-// vertex.  Closing is inline from the atomic's return value wherever one atomic returns
-// every count of the end vertex:
-//   (2,k) W16: u16 b1 | u16 b2 per end vertex (deg u <= 65535), W32: two words; adding a
-//        wedge to a bucket holding c adds C(c, k-1) = C(c+1, k) - C(c, k);
-//   classify C10: pp | mm << 10 | pm << 20 (deg u <= 1023): adding a pp wedge to (a, b, d)
-//        adds a to C(pp,2), b to pp*mm and d to pp*pm (likewise for mm and pm);
-//   classify C32 (deg u > 1023): three words, no-return increments and a closing sweep.
+// round-robin): the anchor's end-vertex ranks are cut into bands from the top (one band
+// table column per band when the table exists); per band and per batch of <= T records,
+// each record's admitted sub-slice comes from the table or a galloping search, a block
+// scan lays the 32-byte chunks out and the chunk walker (bbc_walk.cuh) increments a
+// shared-memory counter per end vertex:
+//   C10: pp | mm << 10 | pm << 20 (deg u <= 1023), closed inline from the atomic's return
+//        value (adding a pp wedge to (a, b, d) adds a to C(pp,2), b to pp*mm and d to
+//        pp*pm, likewise for mm and pm), or -- dense bands -- by no-return increments and
+//        a sweep;
+//   C32 (deg u > 1023): three words, no-return increments and a closing sweep.
 // Totals are exact 128-bit per thread, reduced with one pair of atomics per warp.
 #include <cstring>
 
@@ -33,7 +28,7 @@ namespace bbc {
 
 namespace {
 
-enum ExtMode { kClassify = 0, kBicliques = 1 };
+enum ExtMode { kClassify = 0 };
 
 struct ExtParams {
   const uint32_t* __restrict__ adj;
@@ -47,7 +42,6 @@ struct ExtParams {
   uint32_t nbands, t16;
   uint32_t n, ntasks, part_index, part_count;
   uint32_t cap_words;
-  uint32_t k1;  // (2,k): k - 1
   int dynamic;
   unsigned long long* acc;  // 6 x (lo, hi) + [12] overflow flag
   unsigned int* queue;
@@ -58,49 +52,6 @@ __device__ __forceinline__ void add128(unsigned long long& lo, unsigned long lon
   lo += x;
   hi += (lo < x) ? 1ull : 0ull;
 }
-
-// C(c, j) for c >= j >= 1, exact below 2^64; ~0 (the overflow marker) above
-__device__ __forceinline__ unsigned long long binom_dev(unsigned long long c, uint32_t j) {
-  unsigned __int128 r = 1;
-  if ((unsigned long long)j > c - j) j = (uint32_t)(c - j);
-  for (uint32_t i = 1; i <= j; ++i) {
-    r = r * (unsigned __int128)(c - j + i) / i;
-    if (r >> 64) return ~0ull;
-  }
-  return (unsigned long long)r;
-}
-
-// the ops keep their partial sums as members (registers once inlined); the caller adds
-// them to its 128-bit totals after the walk
-
-// (2,k), u16 b1 | u16 b2 per end vertex; rb rebased by lo_rank * 4
-struct OpBiclW16 {
-  uint32_t rb, k1;
-  unsigned long long lo = 0, hi = 0;
-  uint32_t ovf = 0;
-  __device__ __forceinline__ void add(uint32_t c) {
-    // C(c, k-1) for c >= k-1; closed forms for k = 2, 3 (exact in 64 bits for c < 2^32)
-    const unsigned long long cc = c;
-    const unsigned long long x = k1 == 1u ? cc : k1 == 2u ? (cc * (cc - 1ull)) >> 1 : binom_dev(c, k1);
-    if (x == ~0ull) ovf = 1u;
-    lo += x;
-    hi += (lo < x) ? 1ull : 0ull;
-  }
-  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
-    const uint32_t sh = ((w ^ sg) >> 27) & 16u;
-    const uint32_t c = (s_atom_add(rb + (w << 2), 1u << sh) >> sh) & 0xffffu;
-    if (c >= k1) add(c);
-  }
-  __device__ __forceinline__ void flush() {}
-};
-
-// (2,k), two u32 words per end vertex; rb rebased by lo_rank * 8
-struct OpBiclW32 : OpBiclW16 {
-  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
-    const uint32_t c = s_atom_add(rb + (w << 3) + (((w ^ sg) >> 29) & 4u), 1u);
-    if (c >= k1) add(c);
-  }
-};
 
 // wedge class: 0 pp, 1 mm, 2 pm (sg = s(u, c) in bit 31, word bit 31 = s(c, w))
 __device__ __forceinline__ uint32_t wedge_class(uint32_t w, uint32_t sg) {
@@ -132,27 +83,15 @@ struct OpClsC10 {
   __device__ __forceinline__ void flush() {}
 };
 
-// dense packed bands (>= 2 wedges per counter word): no-return increments, closed by the
-// sweep -- (2,k) u16 b1 | u16 b2, classification pp | mm << 10 | pm << 20
-template <int MODE>
+// dense packed bands (>= 2 wedges per counter word): no-return increments of
+// pp | mm << 10 | pm << 20, closed by the sweep
 struct OpPackedDense {
   uint32_t rb;
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
-    if (MODE == kBicliques)
-      s_red_add(rb + (w << 2), 1u << (((w ^ sg) >> 27) & 16u));
-    else
-      s_red_add(rb + (w << 2), 1u << (10u * wedge_class(w, sg)));
+    s_red_add(rb + (w << 2), 1u << (10u * wedge_class(w, sg)));
   }
   __device__ __forceinline__ void flush() {}
 };
-
-// C(c, k) for the sweep (closed forms for k = 2, 3; c < 2^16 keeps them exact in 64 bits)
-__device__ __forceinline__ unsigned long long binom_k(unsigned long long c, uint32_t k) {
-  if (c < k) return 0ull;
-  if (k == 2u) return (c * (c - 1ull)) >> 1;
-  if (k == 3u) return c * (c - 1ull) * (c - 2ull) / 6ull;
-  return binom_dev(c, k);
-}
 
 // classification, three u32 words per end vertex, closed by the sweep; rb rebased by
 // lo_rank * 12
@@ -180,8 +119,8 @@ template <int T, int MODE>
 __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uint32_t rb, uint32_t re,
                            unsigned long long (&acc)[12], uint32_t& ovf, unsigned long long& work) {
   const uint32_t deg = re - rb;
-  const bool wide = MODE == kClassify ? deg > 1023u : deg > 65535u;
-  const uint32_t wpv = wide ? (MODE == kClassify ? 3u : 2u) : 1u;  // words per end vertex
+  const bool wide = deg > 1023u;
+  const uint32_t wpv = wide ? 3u : 1u;  // words per end vertex
   const bool cols = !wide && P.bnd != nullptr && P.t16 > 0u && P.t16 <= P.cap_words;
   const uint32_t span = cols ? P.t16 : P.cap_words / wpv;
   const uint32_t nbands = (P.n - 1u - r) / span + 1u;  // bands 0..nbands-1 hold ranks > r
@@ -237,29 +176,11 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
       __syncthreads();
       work += myw;
       band_w += bw;
-      if (dense < 0) dense = (wide && MODE == kClassify) || (!wide && bw * nbatch >= 2ull * band_words);
+      if (dense < 0) dense = wide || bw * nbatch >= 2ull * band_words;
       if (ngroups) {
         if (dense && !wide) {
-          OpPackedDense<MODE> op{base - (lo_rank << 2)};
+          OpPackedDense op{base - (lo_rank << 2)};
           walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
-        } else if (MODE == kBicliques) {
-          OpBiclW16 x;
-          if (!wide) {
-            OpBiclW16 op;
-            op.rb = base - (lo_rank << 2);
-            op.k1 = P.k1;
-            walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
-            x = op;
-          } else {
-            OpBiclW32 op;
-            op.rb = base - (lo_rank << 3);
-            op.k1 = P.k1;
-            walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
-            x = op;
-          }
-          add128(acc[0], acc[1], x.lo);
-          acc[1] += x.hi;
-          ovf |= x.ovf;
         } else if (!wide) {
           OpClsC10 op;
           op.rb = base - (lo_rank << 2);
@@ -281,7 +202,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
     uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
     const uint32_t nq = (band_words + 3u) / 4u;
     if (dense) {
-      if (MODE == kClassify && wide) {
+      if (wide) {
         // closing sweep over (pp, mm, pm) triples
         for (uint32_t i = threadIdx.x; i < (band_words / 3u); i += T) {
           const unsigned long long a = S.cnt[3u * i], bb = S.cnt[3u * i + 1u], d = S.cnt[3u * i + 2u];
@@ -292,7 +213,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
           part[4] += a * d;
           part[5] += bb * d;
         }
-      } else if (MODE == kClassify) {
+      } else {
         for (uint32_t i = threadIdx.x; i < band_words; i += T) {
           const uint32_t x = S.cnt[i];
           if (x == 0u) continue;
@@ -304,16 +225,6 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
           part[4] += a * d;
           part[5] += bb * d;
         }
-      } else {
-        const uint32_t k = P.k1 + 1u;
-        for (uint32_t i = threadIdx.x; i < band_words; i += T) {
-          const uint32_t x = S.cnt[i];
-          if (x == 0u) continue;
-          const unsigned long long v = binom_k(x & 0xffffu, k), w = binom_k(x >> 16, k);
-          if (v == ~0ull || w == ~0ull) ovf = 1u;
-          add128(acc[0], acc[1], v);
-          add128(acc[0], acc[1], w);
-        }
       }
       __syncthreads();
     }
@@ -321,8 +232,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
     for (uint32_t i = threadIdx.x; i < nq; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
   }
-  if (MODE == kClassify)
-    for (int i = 0; i < 6; ++i) add128(acc[2 * i], acc[2 * i + 1], part[i]);
+  for (int i = 0; i < 6; ++i) add128(acc[2 * i], acc[2 * i + 1], part[i]);
 }
 
 template <int T, int MINB, int MODE>
@@ -361,7 +271,7 @@ __global__ void __launch_bounds__(T, MINB) k_ext(ExtParams P) {
   }
   // exact reduction: warp shuffle of the 128-bit values, one pair of atomics per warp
   const int lane = threadIdx.x & 31;
-  constexpr int kVals = MODE == kClassify ? 6 : 1;
+  constexpr int kVals = 6;
 #pragma unroll
   for (int i = 0; i < kVals; ++i) {
     unsigned long long lo = acc[2 * i], hi = acc[2 * i + 1];
@@ -426,7 +336,6 @@ int ext_launch(Graph& g, const bbc_opts& opts, uint32_t k, unsigned long long* h
   P.part_index = (uint32_t)opts.part_index;
   P.part_count = (uint32_t)part_count;
   P.cap_words = (uint32_t)cap_words;
-  P.k1 = k - 1u;
   P.dynamic = opts.algo == BBC_ALGO_GBBCPP;
   P.acc = g.acc;
   P.queue = g.queue;
@@ -497,30 +406,6 @@ int classify_graph(Graph& g, const bbc_opts* o, uint64_t out[12], bbc_stats* st)
   if (int rc = ext_launch<kClassify>(g, opts, 2u, h, &ms, &blocks)) return rc;
   for (int i = 0; i < 12; ++i) out[i] = h[i];
   ext_stats(g, st, blocks, ms);
-  return BBC_OK;
-}
-
-int count_2k_graph(Graph& g, int32_t k, const bbc_opts* o, uint64_t out[2], bbc_stats* st) {
-  bbc_opts opts{};
-  if (o) opts = *o;
-  if (k < 2) {
-    set_error("k must be >= 2, got " + std::to_string(k));
-    return BBC_ERR_ARG;
-  }
-  if (int rc = ext_check_opts(opts)) return rc;
-  BBC_CK(cudaSetDevice(g.device));
-  unsigned long long h[13];
-  float ms = 0.f;
-  int blocks = 0;
-  if (int rc = ext_launch<kBicliques>(g, opts, (uint32_t)k, h, &ms, &blocks)) return rc;
-  out[0] = h[0];
-  out[1] = h[1];
-  ext_stats(g, st, blocks, ms);
-  if (st) st->balanced_hi = h[1];
-  if (h[1] || h[12]) {
-    set_error("balanced (2,k) count exceeded 64-bit range");
-    return BBC_ERR_OVERFLOW;
-  }
   return BBC_OK;
 }
 

@@ -54,8 +54,7 @@ struct Graph {
                            // walked groups, walked wedges, round setups
   int num_sms = 0;
   int max_smem = 0;
-  int minb = 8;       // 128-thread CTAs per SM (env BBC_MINB: 4 / 6 / 8 / 10 / 12)
-  int threads = 128;  // count-kernel CTA size (128 / 256 / 512 / 1024; env BBC_THREADS)
+  int threads = 128;  // count-kernel CTA size (128, or 256 for experiments: env BBC_THREADS)
   float preprocess_ms = 0.f;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };

@@ -540,9 +540,8 @@ int init_handle(Graph& g, int device, int64_t n_u, int64_t n_v, int64_t m) {
   BBC_CK(cudaDeviceGetAttribute(&g.max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   if (const char* e = std::getenv("BBC_THREADS")) {
     int t = std::atoi(e);
-    if (t == 128 || t == 256 || t == 512 || t == 1024) g.threads = t;
+    if (t == 128 || t == 256) g.threads = t;
   }
-  if (const char* e = std::getenv("BBC_MINB")) g.minb = std::atoi(e);
   BBC_CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
   {
     cudaMemPool_t pool;

@@ -140,6 +140,38 @@ __device__ __forceinline__ void s_st(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
+// C(c, j) exactly, ~0 (an overflow marker) from 2^64 - 1 on
+__device__ __forceinline__ unsigned long long binom_sat(unsigned long long c, uint32_t j) {
+  if ((unsigned long long)j > c) return 0ull;
+  if ((unsigned long long)j > c - j) j = (uint32_t)(c - j);
+  unsigned __int128 r = 1;
+  for (uint32_t i = 1; i <= j; ++i) {
+    r = r * (unsigned __int128)(c - j + i) / i;
+    if (r >> 64) return ~0ull;
+  }
+  return r == (unsigned __int128)~0ull ? ~0ull : (unsigned long long)r;
+}
+
+// C(c, k) with closed forms for k = 1, 2, 3 (exact below 2^21 for k = 3)
+__device__ __forceinline__ unsigned long long binom_k(unsigned long long c, uint32_t k) {
+  if (c < k) return 0ull;
+  if (k == 1u) return c;
+  if (k == 2u) return (c * (c - 1ull)) >> 1;
+  if (k == 3u && c < (1ull << 21)) return c * (c - 1ull) * (c - 2ull) / 6ull;
+  return binom_sat(c, k);
+}
+
+// 128-bit accumulation (lo, hi) of a binom_k value; the overflow marker adds 2^64, so any
+// total that passed 2^64 - 1 shows in the high word
+__device__ __forceinline__ void add_k(unsigned long long& lo, unsigned long long& hi, unsigned long long x) {
+  if (x == ~0ull) {
+    hi += 1ull;
+    return;
+  }
+  lo += x;
+  hi += (lo < x) ? 1ull : 0ull;
+}
+
 // 256-bit streaming load (sm_100: LDG.E.NA.ENL2.256), no L1 allocation
 __device__ __forceinline__ void ld_stream8(const uint32_t* p, uint32_t (&r)[8]) {
   asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
