@@ -71,3 +71,46 @@ def test_other_configs_scaled_invariants(gpu, key):
             out.add((r.balanced, r.unbalanced))
         g.close()
     assert len(out) == 1
+
+
+def test_wide_sparse_ranges_all_cold_strategies_agree(gpu):
+    """Config 4's recipe at 1/10 size (2.5 M anchors, cold rank ranges of millions): the
+    key-hash rounds (default there), bitmap rounds only (flags bit 1), counter tiles only
+    (bit 7), forced hash rounds (bit 13) and the general banded path give one answer, on
+    both sides and for every partition."""
+    cfg = synth.CONFIGS[4].scaled(0.1)
+    u, v, s = synth.generate(cfg)
+    g = DeviceGraph.from_host(cfg.n_u, cfg.n_v, u, v, s)
+    out = {f: g.count(ALGO_GBBCPP, flags=f) for f in (0, 2, 128, 8192, _lib.FLAG_BANDED_ONLY)}
+    ref = (out[0].balanced, out[0].unbalanced)
+    assert all((r.balanced, r.unbalanced) == ref for r in out.values()), {f: (r.balanced, r.unbalanced)
+                                                                         for f, r in out.items()}
+    assert all(r.wedges == g.w_s for r in out.values())
+    parts = [g.count(ALGO_GBBC, part_index=p, part_count=3) for p in range(3)]
+    assert (sum(p.balanced for p in parts), sum(p.unbalanced for p in parts)) == ref
+    g.close()
+    gu = DeviceGraph.from_host(cfg.n_u, cfg.n_v, u, v, s, 0, SIDE_U if g.anchor_side == 1 else SIDE_V)
+    r = gu.count()
+    assert (r.balanced, r.unbalanced) == ref
+    gu.close()
+
+
+@pytest.mark.slow
+def test_config3_full_size_invariants(gpu):
+    """Hub-heavy config 3 at full size (100 M edges, planted degree-1e6 hubs on both sides):
+    sides, algorithms and partitions agree; total = all-positive balanced count."""
+    cfg = synth.CONFIGS[3]
+    u, v, s = synth.generate(cfg)
+    res = set()
+    for side in (SIDE_U, SIDE_V):
+        g = DeviceGraph.from_host(cfg.n_u, cfg.n_v, u, v, s, 0, side)
+        for algo in (ALGO_GBBC, ALGO_GBBCPP):
+            r = g.count(algo)
+            res.add((r.balanced, r.unbalanced))
+        g.close()
+    assert len(res) == 1
+    bal, unb = res.pop()
+    gp = DeviceGraph.from_host(cfg.n_u, cfg.n_v, u, v, np.ones_like(s))
+    rp = gp.count()
+    gp.close()
+    assert rp.unbalanced == 0 and rp.balanced == bal + unb
