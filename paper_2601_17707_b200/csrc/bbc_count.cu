@@ -95,6 +95,9 @@ struct OpTileDense {
     else
       s_red_add(rb + ((w << 2) & 0xfffffffcu), 1u << ((v >> 27) & 16u));
   }
+  __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
+    chunk_by_wedge(*this, wv, sg, m);
+  }
   __device__ __forceinline__ void flush() {}
 };
 
@@ -103,6 +106,9 @@ struct OpTileDense32 {
   uint32_t rb;
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
     s_red_add(rb + (w << 3) + (((w ^ sg) >> 29) & 4u), 1u);
+  }
+  __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
+    chunk_by_wedge(*this, wv, sg, m);
   }
   __device__ __forceinline__ void flush() {}
 };
@@ -141,6 +147,9 @@ struct OpTileClose {
       add((old >> sh) & 0xffffu, (old >> (sh ^ 16u)) & 0xffffu);
       if (KEEP) touched[j] = a;
     }
+  }
+  __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
+    chunk_by_wedge(*this, wv, sg, m);
   }
   __device__ __forceinline__ void flush() {
     if (!KG) {
@@ -193,6 +202,9 @@ struct OpKeys {
       h = (h + 1u == K) ? 0u : h + 1u;
     }
   }
+  __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
+    chunk_by_wedge(*this, wv, sg, m);
+  }
   __device__ __forceinline__ void flush() {}
 };
 
@@ -210,18 +222,32 @@ struct OpKeys {
 // walk) and every repeated end vertex is closed (first wedge from the parity bit), so the
 // adjacency is read once.  A round whose queue overflows is redone narrower.
 struct OpBits {
-  uint32_t rb, queue, count, Q;
-  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
-    // bits = (1 | neg << 16) << i with neg = parity of (w ^ sg); (sg >> 15) | 1 is the same
-    // for the whole chunk, so per wedge: shift, one LOP3, shift
-    const uint32_t i = w & 15u;
-    const uint32_t bits = (((w >> 15) & 0x10000u) ^ ((sg >> 15) | 1u)) << i;
-    const uint32_t old = s_atom_or(rb + ((w >> 2) & 0x0ffffffcu), bits);
-    if (old & bits & 0xffffu) {  // seen before: a repeat
-      // counted as negative only if it is negative and the parity bit was already set
-      const uint32_t cneg = ((old & bits) >> 16) != 0u;
-      const uint32_t idx = s_atom_add(count, 1u);
-      if (idx < Q) s_st(queue + (idx << 2), (w & 0x7fffffffu) | (cneg << 31));
+  uint32_t rb, queue, count, Q, dummy;  // dummy: a bitmap word of this lane (ORed with 0)
+  // bits = (1 | neg << 16) << i with neg = parity of (w ^ sg); (sg >> 15) | 1 is the same
+  // for the whole chunk.  The eight atomics issue back to back (an invalid slot ORs 0 into
+  // the dummy word); the rare repeats are queued afterwards.
+  __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
+    const uint32_t sgs1 = (sg >> 15) | 1u;
+    uint32_t old[8], bits[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t w = wv[j];
+      const bool ok = (m >> j) & 1u;
+      bits[j] = ok ? (((w >> 15) & 0x10000u) ^ sgs1) << (w & 15u) : 0u;
+      old[j] = s_atom_or(ok ? rb + ((w >> 2) & 0x0ffffffcu) : dummy, bits[j]);
+    }
+    uint32_t rep = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) rep |= ((old[j] & bits[j] & 0xffffu) != 0u ? 1u : 0u) << j;
+    if (rep) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (!((rep >> j) & 1u)) continue;
+        // counted as negative only if it is negative and the parity bit was already set
+        const uint32_t cneg = ((old[j] & bits[j]) >> 16) != 0u;
+        const uint32_t idx = s_atom_add(count, 1u);
+        if (idx < Q) s_st(queue + (idx << 2), (wv[j] & 0x7fffffffu) | (cneg << 31));
+      }
     }
   }
   __device__ __forceinline__ void flush() {}
@@ -598,7 +624,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       uint32_t* queue = S.cnt + span_words;
       uint32_t* keys = queue + Q;
       uint32_t* vals = keys + K;
-      OpBits op{sptr(bm) - ((lo_rank >> 4) << 2), sptr(queue), sptr(cnt), Q};
+      OpBits op{sptr(bm) - ((lo_rank >> 4) << 2), sptr(queue), sptr(cnt), Q, sptr(bm) + ((threadIdx.x & 31u) << 2)};
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ng, op);
       __syncthreads();
       const uint32_t nq = *cnt;

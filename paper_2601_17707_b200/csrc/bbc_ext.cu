@@ -80,6 +80,9 @@ struct OpClsC10 {
       c5 += b;
     }
   }
+  __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
+    chunk_by_wedge(*this, wv, sg, m);
+  }
   __device__ __forceinline__ void flush() {}
 };
 
@@ -90,6 +93,9 @@ struct OpPackedDense {
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
     s_red_add(rb + (w << 2), 1u << (10u * wedge_class(w, sg)));
   }
+  __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
+    chunk_by_wedge(*this, wv, sg, m);
+  }
   __device__ __forceinline__ void flush() {}
 };
 
@@ -99,6 +105,9 @@ struct OpClsC32 {
   uint32_t rb;
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
     s_red_add(rb + (w & 0x7fffffffu) * 12u + 4u * wedge_class(w, sg), 1u);
+  }
+  __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
+    chunk_by_wedge(*this, wv, sg, m);
   }
   __device__ __forceinline__ void flush() {}
 };

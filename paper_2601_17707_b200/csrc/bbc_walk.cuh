@@ -179,6 +179,14 @@ __device__ __forceinline__ void ld_stream8(const uint32_t* p, uint32_t (&r)[8]) 
                : "l"(p));
 }
 
+// default chunk handler: op.wedge(word, sign, slot) for every valid slot
+template <class Op>
+__device__ __forceinline__ void chunk_by_wedge(Op& op, const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (m & (1u << j)) op.wedge(wv[j], sg, j);
+}
+
 // The walk unit: an aligned 32-byte chunk of 8 adjacency words.  A sub-slice [lo, hi)
 // covers chunks lo / 8 .. (hi - 1) / 8.  (adj is 256-byte aligned and padded by 8 words.)
 __device__ __forceinline__ uint32_t unit_count(uint32_t lo, uint32_t hi) { return ((hi + 7u) >> 3) - (lo >> 3); }
@@ -193,7 +201,9 @@ __device__ __forceinline__ uint32_t slot_mask8(uint32_t p0, uint32_t lo, uint32_
 // Walk the 32-byte chunks of the round's sub-slices, one chunk (8 wedges) per thread per
 // iteration: one fixed-depth record search and one 256-bit load per chunk; consecutive
 // threads take consecutive chunks of a record (a warp reads 1 KB contiguous).
-// op.wedge(word, sign, slot) runs for every valid wedge; op.flush() after each chunk.
+// op.chunk(words, sign, valid-slot mask) handles the chunk (ops that can are branch-free:
+// an invalid slot becomes a no-op atomic on a dummy word, so all eight shared-memory
+// atomics issue back to back); op.flush() after each chunk.
 template <int T, class Op>
 __device__ __forceinline__ void walk_chunks(const uint32_t* adj, const uint32_t* s_lo, const uint32_t* s_hi,
                                             const uint32_t* s_pfx, int nb, uint32_t nunits, Op& op) {
@@ -209,9 +219,7 @@ __device__ __forceinline__ void walk_chunks(const uint32_t* adj, const uint32_t*
     uint32_t wv[8];
     ld_stream8(adj + p0, wv);
     const uint32_t m = slot_mask8(p0, lo, hi);
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (m & (1u << j)) op.wedge(wv[j], sg, j);
+    op.chunk(wv, sg, m);
     op.flush();
   }
 }
