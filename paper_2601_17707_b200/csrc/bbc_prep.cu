@@ -67,7 +67,7 @@ __device__ __forceinline__ void validate_edge(int64_t i, int32_t uu, int32_t vv,
 // Four edges per thread with 16-byte loads of u / v and one 4-byte load of signs when the
 // arrays are 16-byte aligned (the tail and unaligned inputs go edge by edge).
 __global__ void k_validate_degrees(const int32_t* __restrict__ u, const int32_t* __restrict__ v,
-                                   const int8_t* __restrict__ s, int64_t m, int64_t n_u, int64_t n_v,
+                                   const int8_t* __restrict__ s, int64_t m, int64_t base, int64_t n_u, int64_t n_v,
                                    unsigned int* __restrict__ deg_u, unsigned int* __restrict__ deg_v,
                                    unsigned long long* __restrict__ err) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
@@ -79,14 +79,15 @@ __global__ void k_validate_degrees(const int32_t* __restrict__ u, const int32_t*
     for (int64_t q = tid; q < m4; q += nt) {
       const int4 u4 = reinterpret_cast<const int4*>(u)[q], v4 = reinterpret_cast<const int4*>(v)[q];
       const int32_t s4 = reinterpret_cast<const int32_t*>(s)[q];
-      validate_edge(4 * q + 0, u4.x, v4.x, (int8_t)(s4 & 0xff), n_u, n_v, deg_u, deg_v, err);
-      validate_edge(4 * q + 1, u4.y, v4.y, (int8_t)((s4 >> 8) & 0xff), n_u, n_v, deg_u, deg_v, err);
-      validate_edge(4 * q + 2, u4.z, v4.z, (int8_t)((s4 >> 16) & 0xff), n_u, n_v, deg_u, deg_v, err);
-      validate_edge(4 * q + 3, u4.w, v4.w, (int8_t)(s4 >> 24), n_u, n_v, deg_u, deg_v, err);
+      validate_edge(base + 4 * q + 0, u4.x, v4.x, (int8_t)(s4 & 0xff), n_u, n_v, deg_u, deg_v, err);
+      validate_edge(base + 4 * q + 1, u4.y, v4.y, (int8_t)((s4 >> 8) & 0xff), n_u, n_v, deg_u, deg_v, err);
+      validate_edge(base + 4 * q + 2, u4.z, v4.z, (int8_t)((s4 >> 16) & 0xff), n_u, n_v, deg_u, deg_v, err);
+      validate_edge(base + 4 * q + 3, u4.w, v4.w, (int8_t)(s4 >> 24), n_u, n_v, deg_u, deg_v, err);
     }
     done = m4 * 4;
   }
-  for (int64_t i = done + tid; i < m; i += nt) validate_edge(i, u[i], v[i], s[i], n_u, n_v, deg_u, deg_v, err);
+  for (int64_t i = done + tid; i < m; i += nt)
+    validate_edge(base + i, u[i], v[i], s[i], n_u, n_v, deg_u, deg_v, err);
 }
 
 // sum C(d, 2) and max d over one degree array
@@ -294,7 +295,16 @@ void free_graph_arrays(Graph& g) {
 }
 
 // Full pipeline on device arrays.  Returns a bbc_status.
-int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t* ds, int side_rule) {
+// Host edge arrays to upload into the device buffers during the build (chunked, each
+// chunk validated while the next one is copied).
+struct Upload {
+  const int32_t* u;
+  const int32_t* v;
+  const int8_t* s;
+};
+
+int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t* ds, int side_rule,
+                    const Upload* up = nullptr) {
   cudaStream_t st = g.stream;
   const int64_t m = g.m, n_u = g.n_u, n_v = g.n_v;
   const int sms = g.num_sms;
@@ -311,9 +321,37 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
   BBC_CK(cudaMemsetAsync(deg_v.p, 0, (size_t)(n_v + 1) * 4, st));
   BBC_CK(cudaMemsetAsync(scal.p, 0, 64, st));
   BBC_CK(cudaMemsetAsync(scal.p, 0xff, 16, st));
-  if (m > 0)
-    k_validate_degrees<<<grid_for(m, sms), kThreads, 0, st>>>(du, dv, ds, m, n_u, n_v, deg_u.as<unsigned int>(),
+  if (m > 0 && up) {
+    // the upload runs on a copy stream in chunks; chunk i is validated on the build stream
+    // as soon as it has landed, overlapping the copy of chunk i + 1
+    cudaStream_t cs;
+    BBC_CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaEvent_t ready;
+    BBC_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    BBC_CK(cudaEventRecord(ready, st));  // the upload buffers were allocated on st
+    BBC_CK(cudaStreamWaitEvent(cs, ready, 0));
+    cudaEventDestroy(ready);
+    const int64_t nch = m >= (1ll << 22) ? 8 : 1;
+    const int64_t chunk = ((m + nch - 1) / nch + 3) & ~3ll;  // multiples of 4 keep the vector loads aligned
+    for (int64_t off = 0; off < m; off += chunk) {
+      const int64_t len = std::min(chunk, m - off);
+      BBC_CK(cudaMemcpyAsync((void*)(du + off), up->u + off, (size_t)len * 4, cudaMemcpyHostToDevice, cs));
+      BBC_CK(cudaMemcpyAsync((void*)(dv + off), up->v + off, (size_t)len * 4, cudaMemcpyHostToDevice, cs));
+      BBC_CK(cudaMemcpyAsync((void*)(ds + off), up->s + off, (size_t)len, cudaMemcpyHostToDevice, cs));
+      cudaEvent_t ev;
+      BBC_CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      BBC_CK(cudaEventRecord(ev, cs));
+      BBC_CK(cudaStreamWaitEvent(st, ev, 0));
+      cudaEventDestroy(ev);
+      k_validate_degrees<<<grid_for(len, sms), kThreads, 0, st>>>(du + off, dv + off, ds + off, len, off, n_u, n_v,
+                                                                  deg_u.as<unsigned int>(), deg_v.as<unsigned int>(),
+                                                                  d_err);
+    }
+    cudaStreamDestroy(cs);
+  } else if (m > 0) {
+    k_validate_degrees<<<grid_for(m, sms), kThreads, 0, st>>>(du, dv, ds, m, 0, n_u, n_v, deg_u.as<unsigned int>(),
                                                               deg_v.as<unsigned int>(), d_err);
+  }
   // W_U = sum over V of C(deg_v, 2) (anchoring U), W_V = sum over U of C(deg_u, 2)
   k_wedge_sum<<<grid_for(n_v, sms), kThreads, 0, st>>>(deg_v.as<unsigned int>(), n_v, d_wsum + 0, d_max + 1);
   k_wedge_sum<<<grid_for(n_u, sms), kThreads, 0, st>>>(deg_u.as<unsigned int>(), n_u, d_wsum + 1, d_max + 0);
@@ -591,19 +629,15 @@ int create_common(int device, int64_t n_u, int64_t n_v, int64_t m, const int32_t
     rc = alloc(&du.p, (size_t)m * 4);
     if (!rc) rc = alloc(&dv.p, (size_t)m * 4);
     if (!rc) rc = alloc(&ds.p, (size_t)m);
-    if (!rc) {
-      cudaError_t e = cudaMemcpyAsync(du.p, u, (size_t)m * 4, cudaMemcpyHostToDevice, g.stream);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(dv.p, v, (size_t)m * 4, cudaMemcpyHostToDevice, g.stream);
-      if (e == cudaSuccess) e = cudaMemcpyAsync(ds.p, s, (size_t)m, cudaMemcpyHostToDevice, g.stream);
-      if (e != cudaSuccess) rc = cuda_fail(e, "host-to-device edge upload");
-    }
     pu = du.as<int32_t>();
     pv = dv.as<int32_t>();
     ps = ds.as<int8_t>();
   }
   if (!rc) {
+    // device time of the build; with host arrays it includes their (overlapped) upload
     cudaEventRecord(t0, g.stream);
-    rc = build_on_device(g, pu, pv, ps, side_rule);
+    const Upload up{u, v, s};
+    rc = build_on_device(g, pu, pv, ps, side_rule, host && m > 0 ? &up : nullptr);
     cudaEventRecord(t1, g.stream);
     cudaEventSynchronize(t1);
     cudaEventElapsedTime(&g.preprocess_ms, t0, t1);
