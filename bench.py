@@ -156,10 +156,19 @@ def run_reference(args):
     u, v, s = synth.generate(cfg)
     budget = max(2.0, 150.0 / max(args.steps + args.warmup, 1))
     cb = cpu_port_rate(cfg.n_u, cfg.n_v, u, v, s, budget, steps=args.steps, warmup=args.warmup)
+    from oracle.oracle import OracleGraph
+
+    og = OracleGraph(cfg.n_u, cfg.n_v, u, v, s)
+    w_u, w_v = og.admitted_total(0), og.admitted_total(1)
+    og.close()
+    w_ref = w_u if cfg.n_u <= cfg.n_v else w_v  # the reference's min_side (graph.py:174-176)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": cfg.name, "n_u": cfg.n_u, "n_v": cfg.n_v, "edges": cfg.m, "seed": cfg.seed},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": w_ref / cb["value"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "n_u": cfg.n_u, "n_v": cfg.n_v, "edges": cfg.m, "p_neg": cfg.p_neg,
+                       "gamma": cfg.gamma_u, "seed": cfg.seed, "W_U": w_u, "W_V": w_v,
+                       "ms_per_step_note": "full-graph count time extrapolated from the sampled rate"},
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0},
             "note": "reference = oracle/bbc_oracle.c, a C restatement of the reference's Python bucket engine "
