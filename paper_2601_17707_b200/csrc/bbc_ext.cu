@@ -40,6 +40,7 @@ struct ExtParams {
   const uint32_t* __restrict__ bnd;   // band table (nullptr: searches only)
   const uint32_t* __restrict__ brow;
   uint32_t nbands, t16;
+  uint32_t hash_target;  // wedges per hash round over sparse column ranges (0: bands only)
   uint32_t n, ntasks, part_index, part_count;
   uint32_t cap_words;
   int dynamic;
@@ -112,6 +113,45 @@ struct OpClsC32 {
   __device__ __forceinline__ void flush() {}
 };
 
+// sparse column ranges: a linear-probing hash of K slots, key = rank + 1 in word 2h,
+// packed pp | mm << 10 | pm << 20 counts in word 2h + 1, closed inline from the add's
+// return value like OpClsC10 (a round's wedge count is known before its walk and kept
+// at or below K / 2, so the table never fills)
+struct OpClsHash {
+  uint32_t* tab;
+  uint32_t K;
+  unsigned long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0;
+  __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
+    const uint32_t t = wedge_class(w, sg);
+    const uint32_t key = (w & 0x7fffffffu) + 1u;
+    uint32_t h = (uint32_t)(((unsigned long long)(key * 0x9E3779B1u) * K) >> 32);
+    for (;;) {
+      const uint32_t k = atomicCAS(&tab[2u * h], 0u, key);
+      if (k == 0u || k == key) break;
+      h = (h + 1u == K) ? 0u : h + 1u;
+    }
+    const uint32_t old = atomicAdd(&tab[2u * h + 1u], 1u << (10u * t));
+    const uint32_t a = old & 1023u, b = (old >> 10) & 1023u, d = old >> 20;
+    if (t == 0u) {
+      c0 += a;
+      c1 += b;
+      c4 += d;
+    } else if (t == 1u) {
+      c2 += b;
+      c1 += a;
+      c5 += d;
+    } else {
+      c3 += d;
+      c4 += a;
+      c5 += b;
+    }
+  }
+  __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
+    chunk_by_wedge(*this, wv, sg, m);
+  }
+  __device__ __forceinline__ void flush() {}
+};
+
 struct ExtSmem {
   uint32_t* cnt;
   uint32_t *lo, *hi, *pfx;
@@ -119,11 +159,13 @@ struct ExtSmem {
   unsigned long long* w;
 };
 
-// One anchor: bands from the top, record batches of T.  Packed layouts use one table
-// column per band when the band table exists (bounds from the table, or a galloping search
-// from the previous band's bound); a band holding >= 2 wedges per counter word (estimated
-// from its first batch) is counted with no-return increments and swept, others close
-// inline from the atomics' return values and are cleared with vector stores.
+// One anchor: bands from the top, record batches of T.  Packed layouts use table-column
+// bands when the band table exists (bounds from the table, or a galloping search from the
+// previous band's bound).  A band holding >= 2 wedges per counter word (estimated from its
+// first batch) is counted with no-return increments and swept, others close inline from
+// the atomics' return values and are cleared with vector stores.  For single-batch anchors
+// the bands after the first (the high-degree end vertices) are widened adaptively to hold
+// about K / 2 wedges in a shared-memory hash (OpClsHash): few rounds over sparse ranges.
 template <int T, int MODE>
 __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uint32_t rb, uint32_t re,
                            unsigned long long (&acc)[12], uint32_t& ovf, unsigned long long& work) {
@@ -132,24 +174,30 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
   const uint32_t wpv = wide ? 3u : 1u;  // words per end vertex
   const bool cols = !wide && P.bnd != nullptr && P.t16 > 0u && P.t16 <= P.cap_words;
   const uint32_t span = cols ? P.t16 : P.cap_words / wpv;
-  const uint32_t nbands = (P.n - 1u - r) / span + 1u;  // bands 0..nbands-1 hold ranks > r
+  const uint32_t nbands = (P.n - 1u - r) / span + 1u;  // unit bands 0..nbands-1 hold ranks > r
   const uint32_t nbatch = (deg + T - 1u) / (uint32_t)T;
   const bool single = nbatch == 1u;
+  const bool hashing = cols && single && P.hash_target > 0u;
+  const uint32_t K = (P.cap_words / 2u) & ~3u, target = min(P.hash_target, K / 2u);
   const uint32_t base = sptr(S.cnt);
   uint32_t scan_buf = 0;
   uint32_t carry = 0;  // single batch: this record's upper bound for the next band
+  uint32_t width = 1;  // unit bands per band (hash rounds)
   unsigned long long part[6] = {0, 0, 0, 0, 0, 0};
-  for (uint32_t b = 0; b < nbands; ++b) {
+  for (uint32_t b = 0; b < nbands;) {
+    const uint32_t nbw = (hashing && b > 0) ? min(width, nbands - b) : 1u;
     const long long top = (long long)P.n - (long long)b * span;
-    const long long bot = top - (long long)span;
+    const long long bot = top - (long long)nbw * span;
     const uint32_t lo_rank = bot > 0 ? (uint32_t)bot : 0u;
     const uint32_t band_words = (uint32_t)(top - (long long)lo_rank) * wpv;
     unsigned long long band_w = 0;
     int dense = -1;
+    bool redo = false, hashed = false;
     for (uint32_t b0 = rb; b0 < re; b0 += T) {
       const int nb = (int)min((uint32_t)T, re - b0);
       uint32_t ng = 0;
       unsigned long long myw = 0;
+      uint32_t nlo = 0;
       if ((int)threadIdx.x < nb) {
         const uint2 rr = P.rec[b0 + threadIdx.x];
         const uint32_t begin = rr.x & 0x7fffffffu;
@@ -158,7 +206,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
         if (bi != 0xffffffffu) {
           const uint32_t* row = P.bnd + (size_t)bi * P.nbands;
           hi = __ldg(row + b);
-          lo = b + 1u < P.nbands ? __ldg(row + b + 1u) : 0u;
+          lo = b + nbw < P.nbands ? __ldg(row + b + nbw) : 0u;
         } else {
           if (b == 0)
             hi = __ldg(P.coff + rr.y + 1);
@@ -170,7 +218,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
         }
         lo = max(lo, begin);
         hi = max(hi, lo);
-        carry = lo;
+        nlo = lo;
         if (hi > lo) {
           ng = unit_count(lo, hi);
           myw = hi - lo;
@@ -183,8 +231,32 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
       const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w, scan_buf++);
       if ((int)threadIdx.x < nb) S.pfx[threadIdx.x] = ex;
       __syncthreads();
+      if (hashing && b > 0 && bw > target && nbw > 1u) {  // too many wedges: narrower, no walk
+        width = max(1u, min(nbw / 2u, (uint32_t)((unsigned long long)nbw * target / bw)));
+        redo = true;
+        break;  // (single batch: the record arrays are not reused before the next scan)
+      }
+      carry = nlo;
       work += myw;
       band_w += bw;
+      if (hashing && b > 0 && bw <= target) {
+        hashed = true;
+        if (ngroups) {
+          OpClsHash op;
+          op.tab = S.cnt;
+          op.K = K;
+          walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+          part[0] += op.c0;
+          part[1] += op.c1;
+          part[2] += op.c2;
+          part[3] += op.c3;
+          part[4] += op.c4;
+          part[5] += op.c5;
+        }
+        if (2ull * bw < target) width = min(2u * width, nbands);
+        __syncthreads();
+        break;
+      }
       if (dense < 0) dense = wide || bw * nbatch >= 2ull * band_words;
       if (ngroups) {
         if (dense && !wide) {
@@ -207,8 +279,19 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
       }
       __syncthreads();  // the next batch overwrites the record arrays
     }
+    if (redo) {
+      __syncthreads();  // every warp is done with this set-up's record arrays
+      continue;
+    }
+    b += nbw;
     if (band_w == 0ull) continue;
     uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
+    if (hashed) {
+#pragma unroll 4
+      for (uint32_t i = threadIdx.x; i < K / 2u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+      __syncthreads();
+      continue;
+    }
     const uint32_t nq = (band_words + 3u) / 4u;
     if (dense) {
       if (wide) {
@@ -340,6 +423,7 @@ int ext_launch(Graph& g, const bbc_opts& opts, uint32_t k, unsigned long long* h
   P.brow = g.brow;
   P.nbands = g.nbands;
   P.t16 = g.t16;
+  P.hash_target = (opts.flags & 2) ? 0u : 1024u;  // flags bit 1: table-column bands only
   P.n = n;
   P.ntasks = n > (uint32_t)opts.part_index ? (n - (uint32_t)opts.part_index + part_count - 1) / part_count : 0u;
   P.part_index = (uint32_t)opts.part_index;
