@@ -174,7 +174,8 @@ __device__ __forceinline__ void add_k(unsigned long long& lo, unsigned long long
 
 // 256-bit streaming load (sm_100: LDG.E.NA.ENL2.256), no L1 allocation
 __device__ __forceinline__ void ld_stream8(const uint32_t* p, uint32_t (&r)[8]) {
-  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  // not volatile: a pure load of read-only data, free to be scheduled early
+  asm("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "l"(p));
 }
