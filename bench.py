@@ -354,7 +354,35 @@ def extensions(cfg, du, dv, ds, device) -> dict:
     out["bicliques_k3"] = {"ms": ms, "wedges": gv.w_s, "wedges_per_s": gv.w_s / (ms * 1e-3), "anchor_side": "V",
                            "count": val, "overflow": ovf}
     gv.close()
+    out["loader"] = loader_rate(du, dv, ds)
     return out
+
+
+def loader_rate(du, dv, ds, lines: int = 2_000_000, host_lines: int = 50_000) -> dict:
+    """Device load_graph on the first `lines` edges of the workload
+    written as text ("u<id> v<id> +-1"), wall time incl. the text upload, next to the host
+    pipeline on a smaller prefix."""
+    import numpy as np
+
+    import paper_2601_17707_b200 as bb
+
+    u, v, s = (x[:lines].cpu().numpy() for x in (du, dv, ds))
+    text = "\n".join(np.char.add(np.char.add(np.char.add(np.char.add("u", u.astype(str)), " v"),
+                                             np.char.add(v.astype(str), " ")), s.astype(str)).tolist()) + "\n"
+    data = text.encode("ascii")
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        h = bb.ingest_device(data)
+        times.append(time.perf_counter() - t0)
+        h.close()
+    dev = statistics.median(times)
+    sample = "\n".join(text.split("\n", host_lines)[:host_lines]) + "\n"
+    t0 = time.perf_counter()
+    bb.load_graph(sample)
+    host = time.perf_counter() - t0
+    return {"lines": int(len(u)), "bytes": len(data), "device_s": dev, "device_lines_per_s": len(u) / dev,
+            "host_lines_per_s": host_lines / host, "host_sample_lines": host_lines}
 
 
 def ctypes_create(pu, pv, ps, cfg, device):
