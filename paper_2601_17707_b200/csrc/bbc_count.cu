@@ -1030,7 +1030,10 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st, int
     P.cap_words = (uint32_t)X.cap_words;
     // the fast path needs the fixed column grid (not with TileConfig.tile_size spans) and
     // ranks < 2^30 (rebased word addressing)
-    P.fast = ((opts.flags & 1) || tile_override || g.t16 == 0 || n >= (1u << 30)) ? 0 : 1;
+    P.fast = ((opts.flags & 1) || tile_override || g.t16 == 0 || n >= (1u << 30) ||
+              (uint32_t)X.cap_words < g.t16 + 8u)  // this configuration's tile must hold a column
+                 ? 0
+                 : 1;
     P.fast_max = two_phase ? (uint32_t)std::min(L.threads, Lc.threads) : (uint32_t)X.threads;
     P.hash_thr = (opts.flags & 2) ? 0u : tune.hash_thr;  // flags bit 1: no key-hash rounds
     // cold two-bit bitmap rounds (flags bit 7 disables): the widest round leaves room for
