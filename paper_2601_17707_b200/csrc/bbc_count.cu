@@ -181,8 +181,8 @@ __device__ __forceinline__ void close_pq(unsigned long long p, unsigned long lon
 // many table columns as hold about K / 2 wedges, in a linear-probing hash of K keys
 // (rank + 1, with the parity of the end vertex's FIRST wedge in bit 31).  The first wedge
 // of an end vertex inserts its key; a later one finds it and queues (slot, own parity).
-// After the walk the queue is counted into a parallel array of packed u16 counts and every
-// repeated slot is closed once (first wedge's parity from the key).  The round's wedge
+// After the walk the queue is counted per key slot in a small secondary set of packed u16
+// counts and every repeated slot is closed once (first wedge's parity from the key).  The round's wedge
 // count is known before the walk (block scan), so the hash never fills; a queue overflow
 // redoes the round narrower.
 struct OpKeys {
@@ -688,16 +688,21 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
   // cold range in key-hash rounds over adaptive column ranges (see OpKeys): a round aims
   // at `target` wedges; the first width comes from the cold range's average density
   auto hash_rounds = [&](unsigned long long wc) {
+    // keys (K words: rank + 1 with the first wedge's parity), the repeat queue (Q), and a
+    // small secondary set (2Q slots) counting repeats per key slot -- only repeated keys
+    // need counts, so the primary set spends one word per slot and holds more wedges
     const uint32_t Q = (P.cap_words / 16u) & ~3u;
-    const uint32_t K = ((P.cap_words - Q) / 2u) & ~3u;
+    const uint32_t SS = 2u * Q;
+    const uint32_t K = (P.cap_words - Q - 2u * SS) & ~3u;
     const uint32_t target = K / 2u;
     const uint32_t span = ncols - hstep;
     uint32_t cols = (uint32_t)max(1ull, min((unsigned long long)span, (unsigned long long)target * span / max(wc, 1ull)));
     uint32_t hi = c1;
     uint32_t parity = 0;
     uint32_t* keys = S.cnt;
-    uint32_t* cnts = keys + K;
-    uint32_t* queue = cnts + K;
+    uint32_t* queue = keys + K;
+    uint32_t* skeys = queue + Q;
+    uint32_t* svals = skeys + SS;
     for (uint32_t c = hstep; c < ncols;) {
       const uint32_t cb = min(c + cols, ncols);
       const uint32_t lo = col(cb, hi);
@@ -730,21 +735,24 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       const uint32_t nq = *cnt;
       const bool ovf = nq > Q;
       if (nq != 0u && !ovf) {
-        // count the repeats per slot; each entry also takes the first wedge's parity
+        // count the repeats per key slot in the secondary set; the entry that inserted the
+        // slot becomes its closer and carries the first wedge's parity
         for (uint32_t i = threadIdx.x; i < nq; i += T) {
           const uint32_t e = queue[i], h = e & 0x7fffffffu;
-          atomicAdd(&cnts[h], (e >> 31) ? 0x10000u : 1u);
-          queue[i] = h | ((keys[h] >> 31) << 30);
+          const uint32_t r = rep_insert(skeys, SS, h + 1u);
+          atomicAdd(&svals[r & 0x7fffffffu], (e >> 31) ? 0x10000u : 1u);
+          queue[i] = (r >> 31) ? ((r & 0x3fffffffu) | 0x80000000u | ((keys[h] >> 31) << 30)) : 0u;
         }
         __syncthreads();
-        // the first entry of a slot to take its counts closes it
         for (uint32_t i = threadIdx.x; i < nq; i += T) {
           const uint32_t e = queue[i];
+          if (e == 0u) continue;
           queue[i] = 0u;
-          const uint32_t v = atomicExch(&cnts[e & 0x3fffffffu], 0u);
-          if (v == 0u) continue;
+          const uint32_t slot = e & 0x3fffffffu, v = svals[slot];
           const unsigned long long neg = (e >> 30) & 1u;
           close_pq<KG>((v & 0xffffu) + (neg ^ 1ull), (v >> 16) + neg, P.k, tb, tu);
+          skeys[slot] = 0u;
+          svals[slot] = 0u;
         }
       } else if (ovf) {
         uint4* q4 = reinterpret_cast<uint4*>(queue);
