@@ -996,7 +996,7 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st, int
 
   // tuning knobs (defaults measured on config 2; env overrides for experiments)
   struct {
-    uint32_t rep_slots = 128, bits_thr = 4096, sweep_min = 2, bm_cols0 = 8, hash_thr = 256;
+    uint32_t rep_slots = 128, bits_thr = 4096, sweep_min = 4, bm_cols0 = 8, hash_thr = 256;
   } tune;
   if (const char* e = std::getenv("BBC_HASH_THR")) tune.hash_thr = (uint32_t)std::atoi(e);
   if (const char* e = std::getenv("BBC_BM_COLS0")) tune.bm_cols0 = (uint32_t)std::atoi(e);
