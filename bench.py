@@ -6,8 +6,10 @@
 Workload (BASELINE.json configs[1]): synthetic Chung-Lu signed bipartite graph, |U| = 1M,
 |V| = 500k, 20M distinct edges, 30 % negative (paper_2601_17707_b200/synth.py, seed 2).
 A "step" is one full count of the graph (G-BBC++ kernel incl. closing) with the CSR
-resident in HBM; under torchrun every rank holds the replicated CSR, counts its share of
-the start vertices and the counters are summed with one NCCL all-reduce.
+resident in HBM; with N ranks (torchrun, or `--gpus N` alone, which re-executes itself
+under torch.distributed.run) rank r uploads edge shard r, the shards are all-gathered
+over NVLink, every rank builds the replicated CSR, counts its share of the start
+vertices, and the counters are summed with one NCCL all-reduce.
 
 JSON line (rank 0): value = W_S / (max over ranks of the device-timed step), W_S the
 admitted wedges of the whole graph; `e2e` = the same metric through the public C ABI
@@ -47,6 +49,10 @@ def parse_args():
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extensions", action="store_true", help="skip the 8(f) classification / (2,k) timings")
+    p.add_argument("--ext-configs", default="3,5",
+                   help="other BASELINE configs timed in `extensions` (G-BBC vs G-BBC++, roofline); '' = none")
+    p.add_argument("--launcher-selftest", action="store_true",
+                   help="spawn/rendezvous check only (gloo, no GPU): rank 0 prints one JSON line")
     return p.parse_args()
 
 
@@ -55,6 +61,51 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def spawn(args) -> int:
+    """`bench.py --gpus N` without a launcher: re-exec under torch.distributed.run with N
+    ranks on 127.0.0.1 (one process per GPU); rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator logging: the ranks NCCL saw
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def launcher_selftest(args) -> int:
+    """The launcher without a GPU: gloo rendezvous, one all-reduce, one JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([rank + 1], dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(t)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"selftest": "launcher", "n_gpus": world, "gpus_requested": args.gpus,
+                          "rank_sum": int(t.item())}), flush=True)
+    return 0
+
+
+def config_dict(cfg, w_u: int, w_v: int, algo: str, world: int) -> dict:
+    """The workload description both arms print (same keys and values)."""
+    side = "U" if w_u <= w_v else "V"
+    return {"workload": cfg.name, "n_u": cfg.n_u, "n_v": cfg.n_v, "edges": cfg.m, "p_neg": cfg.p_neg,
+            "gamma": cfg.gamma_u, "seed": cfg.seed, "anchor_side": side, "W_S": min(w_u, w_v), "W_U": w_u,
+            "W_V": w_v, "algo": algo,
+            "parallelism": f"start-vertex partition x{world}, CSR replicated (sharded upload + all-gather), "
+                           f"counter all-reduce",
+            "l2": f"{L2_FLUSH_BYTES >> 20} MiB buffer overwritten between timed steps"}
 
 
 def measured_peaks() -> dict:
@@ -111,6 +162,16 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return ""
+
+
 def cpu_port_rate(n_u, n_v, u, v, s, budget_s: float, steps: int = 1, warmup: int = 0) -> dict:
     """Time the oracle port (reference bucket engine restated in C) on a bounded anchor sample."""
     from oracle.oracle import OracleGraph
@@ -123,27 +184,20 @@ def cpu_port_rate(n_u, n_v, u, v, s, budget_s: float, steps: int = 1, warmup: in
     t_probe = max(time.perf_counter() - t0, 1e-3)
     est_full = t_probe * probe_stride
     stride = max(1, int(est_full / max(budget_s, 1e-3)) + 1)
-    rates, adm = [], 0
+    rates, secs, adm = [], [], 0
     for i in range(warmup + steps):
         t0 = time.perf_counter()
         r = g.count(side=-1, threads=threads, stride=stride)
         dt = time.perf_counter() - t0
         if i >= warmup:
             rates.append(r.admitted / dt)
+            secs.append(dt)
             adm = r.admitted
     g.close()
-    cpu_model = ""
-    try:
-        for line in Path("/proc/cpuinfo").read_text().splitlines():
-            if line.startswith("model name"):
-                cpu_model = line.split(":", 1)[1].strip()
-                break
-    except Exception:
-        pass
     return {"value": statistics.median(rates), "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"anchors a with a % {stride} == 0 on the reference's min_side ({adm} admitted wedges, "
                       f"reference filter prank[w] < prank[u]); graph build excluded as in cli.py:215",
-            "cpu": cpu_model, "stride": stride}
+            "cpu": cpu_model(), "stride": stride, "sample_wedges": adm, "step_s": statistics.median(secs)}
 
 
 def run_reference(args):
@@ -163,16 +217,16 @@ def run_reference(args):
     og.close()
     w_ref = w_u if cfg.n_u <= cfg.n_v else w_v  # the reference's min_side (graph.py:174-176)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": w_ref / cb["value"] * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["step_s"] * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-            "data": "synthetic",
-            "config": {"workload": cfg.name, "n_u": cfg.n_u, "n_v": cfg.n_v, "edges": cfg.m, "p_neg": cfg.p_neg,
-                       "gamma": cfg.gamma_u, "seed": cfg.seed, "W_U": w_u, "W_V": w_v,
-                       "ms_per_step_note": "full-graph count time extrapolated from the sampled rate"},
+            "data": "synthetic", "config": config_dict(cfg, w_u, w_v, args.algo, args.gpus),
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0},
+            "full_graph_ms_extrapolated": w_ref / cb["value"] * 1e3,
             "note": "reference = oracle/bbc_oracle.c, a C restatement of the reference's Python bucket engine "
-                    "(buckets.py:166-197) pinned to its golden vectors; the Python package is absent on this box"}
+                    "(buckets.py:166-197) pinned to its golden vectors, on every host core; each step counts the "
+                    "anchor sample named in cpu_baseline.sample (ms_per_step is that sample's time, value its "
+                    "admitted wedges / s); the Python package is absent on this box"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -181,27 +235,37 @@ def main():
     args = parse_args()
     if args.impl == "reference":
         return run_reference(args)
-    import numpy as np
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
+    if args.launcher_selftest:
+        return launcher_selftest(args)
     import torch
     import torch.distributed as dist
 
     from paper_2601_17707_b200 import _lib, synth
+    from paper_2601_17707_b200.distributed import build_replicated, shard_bounds
 
     rank, world, local = dist_env()
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = synth.CONFIGS[args.config]
-    u, v, s = synth.generate(cfg)
+    u, v, s = synth.generate(cfg)  # input preparation (host), never timed
     m = cfg.m
+    lo, hi = shard_bounds(m, rank, world)
 
     # ---- device-resident inputs: preprocessing once, then K timed count steps ----
-    du, dv, ds = (torch.from_numpy(x).cuda() for x in (u, v, s))
-    torch.cuda.synchronize()
-    g = _lib.DeviceGraph.from_device_ptrs(cfg.n_u, cfg.n_v, m, du.data_ptr(), dv.data_ptr(), ds.data_ptr(), local)
+    # rank r uploads edge shard r; the shards are all-gathered over NVLink and every rank
+    # builds the replicated CSR (the first build is the cold call: context, pools)
+    t0 = time.perf_counter()
+    g, keep = build_replicated(cfg.n_u, cfg.n_v, m, u[lo:hi], v[lo:hi], s[lo:hi], local)
+    cold_first_call_ms = (time.perf_counter() - t0) * 1e3
+    g.close()
+    g, keep = build_replicated(cfg.n_u, cfg.n_v, m, u[lo:hi], v[lo:hi], s[lo:hi], local)
+    du, dv, ds = keep
+    warm_preprocess_ms = g.count(_lib.ALGO_GBBCPP, part_index=rank, part_count=world).preprocess_ms
     algo = _lib.ALGO_GBBCPP if args.algo == "gbbc++" else _lib.ALGO_GBBC
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
     from paper_2601_17707_b200.distributed import from_limbs, to_limbs
@@ -254,24 +318,29 @@ def main():
     value = w_s / (ms_per_step * 1e-3)
     count_ms_local = sum(times) / args.steps
 
-    # ---- end-to-end through the public C ABI from pinned host buffers ----
-    pu = torch.from_numpy(u).pin_memory()
-    pv = torch.from_numpy(v).pin_memory()
-    ps = torch.from_numpy(s).pin_memory()
+    # ---- end-to-end through the public API from pinned host buffers ----
+    # N = 1: bbc_graph_create(host arrays) + bbc_count; N > 1: this rank's shard uploaded,
+    # NCCL all-gather, bbc_graph_create_device, bbc_count of the partition, all-reduce
+    pu = torch.from_numpy(u[lo:hi] if world > 1 else u).pin_memory()
+    pv = torch.from_numpy(v[lo:hi] if world > 1 else v).pin_memory()
+    ps = torch.from_numpy(s[lo:hi] if world > 1 else s).pin_memory()
     e2e_steps = args.e2e_steps or args.steps
     e2e_times = []
-    e2e_launch = 0
     for i in range(args.warmup + e2e_steps):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        h = ctypes_create(pu, pv, ps, cfg, local)
-        r2 = h.count(algo, part_index=rank, part_count=world)
         if world > 1:
+            h, tmp = build_replicated(cfg.n_u, cfg.n_v, m, pu, pv, ps, local)
+            r2 = h.count(algo, part_index=rank, part_count=world)
             red.copy_(torch.tensor(to_limbs([r2.balanced, r2.unbalanced]), dtype=torch.int64))
             dist.all_reduce(red)
             from_limbs(red.tolist())
+            del tmp
+        else:
+            h = ctypes_create(pu, pv, ps, cfg, local)
+            r2 = h.count(algo)
         dt = time.perf_counter() - t0
         h.close()
         if i >= args.warmup:
@@ -302,19 +371,19 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u32", "data": "synthetic",
-        "config": {"workload": cfg.name, "n_u": cfg.n_u, "n_v": cfg.n_v, "edges": m, "p_neg": cfg.p_neg,
-                   "gamma": cfg.gamma_u, "seed": cfg.seed, "anchor_side": "U" if g.anchor_side == 0 else "V",
-                   "W_S": w_s, "W_U": g.w_u, "W_V": g.w_v, "algo": args.algo,
-                   "parallelism": f"start-vertex partition x{world}, CSR replicated, NCCL all-reduce of counters",
-                   "l2": f"{L2_FLUSH_BYTES >> 20} MiB buffer overwritten between timed steps"},
+        "config": config_dict(cfg, g.w_u, g.w_v, args.algo, world),
         "counts": {"balanced": bal, "unbalanced": unb, "total": bal + unb},
         "count_ms": ms_per_step,
-        "preprocess_ms": r.preprocess_ms,
+        "preprocess_ms": warm_preprocess_ms,
+        "cold_first_call_ms": cold_first_call_ms,
         "wall_s_timed_region": wall,
         "gpu_launches": args.steps,
         "e2e": {"value": w_s / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 9 * m,
-                "d2h_bytes_per_step": 64 + 8 + 32 + 8 * r.blocks, "end_to_end_count_ms": e2e_s * 1e3,
-                "gpu_launches_per_step": e2e_launch, "path": "bbc_graph_create(host arrays) + bbc_count"},
+                "d2h_bytes_per_step": (64 + 8 + 32 + 8 * r.blocks) * world, "end_to_end_count_ms": e2e_s * 1e3,
+                "gpu_launches_per_step": e2e_launch,
+                "path": "bbc_graph_create(host arrays) + bbc_count" if world == 1 else
+                        "per rank: pinned shard upload, NCCL all-gather, bbc_graph_create_device, bbc_count "
+                        "(partition), NCCL all-reduce (max over ranks)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src, "algorithmic_bytes": alg_bytes,
                      "bytes_model": "4*W_S + 12*|E| + 8*|S| (BASELINE.md 2)",
@@ -326,10 +395,16 @@ def main():
     g.close()
     if world == 1 and not args.no_extensions:
         line["extensions"] = extensions(cfg, du, dv, ds, local)
+        ext_cfgs = [int(x) for x in args.ext_configs.split(",") if x.strip()]
+        if ext_cfgs:
+            del du, dv, ds, keep
+            line["extensions"]["configs"] = {str(k): other_config(k, peak, local) for k in ext_cfgs
+                                             if k != args.config}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
     return 0
 
 
@@ -355,6 +430,46 @@ def extensions(cfg, du, dv, ds, device) -> dict:
                            "count": val, "overflow": ovf}
     gv.close()
     out["loader"] = loader_rate(du, dv, ds)
+    return out
+
+
+def other_config(k: int, peak: float, device: int) -> dict:
+    """Another BASELINE config under the bench's clock: G-BBC (static round-robin) and
+    G-BBC++ (dynamic queue) device-timed counts (one warm-up, median of three), the
+    per-CTA load ratio max/mean of each from bbc_block_work (ScheduleReport.max_over_mean,
+    tiled.py:92-97, measured on the device), and the roofline fraction."""
+    import torch
+
+    from paper_2601_17707_b200 import _lib, synth
+
+    cfg = synth.CONFIGS[k]
+    t0 = time.perf_counter()
+    u, v, s = synth.generate(cfg)
+    gen_s = time.perf_counter() - t0
+    g = _lib.DeviceGraph.from_host(cfg.n_u, cfg.n_v, u, v, s, device)
+    del u, v, s
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    out = {"workload": cfg.name, "edges": cfg.m, "anchor_side": "UV"[g.anchor_side], "W_S": g.w_s,
+           "W_U": g.w_u, "W_V": g.w_v, "gen_s": gen_s}
+    alg_bytes = 4 * g.w_s + 12 * cfg.m + 8 * g.n_anchors
+    for name, code in (("gbbc", _lib.ALGO_GBBC), ("gbbc++", _lib.ALGO_GBBCPP)):
+        times = []
+        for i in range(4):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            r = g.count(code)
+            if i:
+                times.append(r.count_ms)
+        work = g.block_work(r.blocks)
+        mean = sum(work) / max(len(work), 1)
+        ms = statistics.median(times)
+        out[name] = {"count_ms": ms, "wedges_per_s": g.w_s / (ms * 1e-3), "balanced": r.balanced,
+                     "unbalanced": r.unbalanced, "cta_work_max_over_mean": max(work) / mean if mean else 1.0,
+                     "blocks": r.blocks,
+                     "roofline_frac": alg_bytes / (ms * 1e-3) / 1e9 / peak}
+    out["counts_agree"] = (out["gbbc"]["balanced"], out["gbbc"]["unbalanced"]) == \
+        (out["gbbc++"]["balanced"], out["gbbc++"]["unbalanced"])
+    g.close()
     return out
 
 

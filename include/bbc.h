@@ -49,7 +49,7 @@ enum bbc_status {
   BBC_ERR_OVERFLOW = 3, /* CountOverflowError (a total exceeds 2^64 - 1)        */
   BBC_ERR_ARG = 4,      /* ValueError (bad sizes, options, sign not +-1)        */
   BBC_ERR_CUDA = 5,     /* BBCountError                                         */
-  BBC_ERR_NCCL = 6,     /* BBCountError (reserved: collectives run host-side)   */
+  BBC_ERR_NCCL = 6,     /* BBCountError (NCCL unavailable / collective failed)  */
   BBC_ERR_NOMEM = 7,    /* BBCountError (device allocation failed)              */
   BBC_ERR_PARSE = 8,    /* MalformedLineError; info = 1-based line               */
   BBC_ERR_MISSING = 9,  /* MissingValueError; info = 1-based line of the edge    */
@@ -165,6 +165,28 @@ int bbc_ingest_edges(bbc_ingest* h, int32_t* u, int32_t* v, int8_t* sign);
 /* Build the counting graph straight from the ingested device arrays. */
 int bbc_ingest_graph(bbc_ingest* h, int32_t side_rule, bbc_graph** out);
 void bbc_ingest_destroy(bbc_ingest* h);
+
+/* several GPUs of this process as the workers of
+ * count_balanced_parallel (buckets.py:213-246: anchors split over workers, exact sum of
+ * the subtotals at :236-243).  bbc_multi_create uploads edge shard i (ceil(m / ndev)
+ * edges) to devices[i] only, all-gathers the shards over NVLink (ncclAllGather), and
+ * builds the replicated CSR on every device; bbc_multi_count counts start-vertex
+ * partition i on devices[i] concurrently and sums the 128-bit (balanced, unbalanced)
+ * with one ncclAllReduce.  Same validation errors as bbc_graph_create; BBC_ERR_NCCL when
+ * libnccl.so.2 is unavailable or a collective fails.  opts.part_count must be 0 / 1. */
+typedef struct bbc_multi bbc_multi;
+int bbc_multi_create(int32_t ndev, const int32_t* devices, int64_t n_u, int64_t n_v, int64_t m,
+                     const int32_t* u, const int32_t* v, const int8_t* sign, int32_t side_rule,
+                     bbc_multi** out);
+int bbc_multi_count(bbc_multi* h, const bbc_opts* opts, uint64_t out[2], bbc_stats* stats);
+/* the handle's devices (returns ndev) and the graph replica on devices[i] */
+int bbc_multi_devices(bbc_multi* h, int32_t* devices, int32_t n);
+bbc_graph* bbc_multi_graph(bbc_multi* h, int32_t i);
+void bbc_multi_destroy(bbc_multi* h);
+/* one-shot create + count + destroy (the SURVEY.md 8(b) proposal, plus side_rule) */
+int bbc_count_multi(int32_t ndev, const int32_t* devices, int64_t n_u, int64_t n_v, int64_t m,
+                    const int32_t* u, const int32_t* v, const int8_t* sign, int32_t side_rule,
+                    const bbc_opts* opts, uint64_t out[2], bbc_stats* stats);
 
 /* Per-CTA admitted wedges of the last bbc_count (ScheduleReport.per_block_work). */
 int bbc_block_work(bbc_graph* g, uint64_t* out, int32_t n);

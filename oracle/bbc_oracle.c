@@ -332,6 +332,131 @@ int bbc_oracle_classify(const og_graph* g, int threads, uint64_t* out) {
   return run(g, 0, threads, 1, 2, 2, out);
 }
 
+/*
+ * The reference's sort_neighbors traversal (count_balanced_2k_serial, buckets.py:87-111):
+ * each centre's list is iterated in ascending priority rank and the scan stops at the
+ * first rank >= prank[u] (:106-107), so scanned = admitted + one stop per record instead
+ * of sum deg(c)^2.  Same b1/b2 buckets and closing as _pair_subtotal (buckets.py:166-197);
+ * buckets are addressed by prank[w] instead of w (a bijection of the end vertices, so the
+ * touched set and the sum over it are unchanged) which turns a scan of a sorted list into
+ * ascending bucket addresses.  b1/b2 are u32 (they are bounded by deg u < 2^32).  Used
+ * for the full-size BASELINE goldens (configs 3-5), where the scan-everything loop above
+ * would take days on the build container.  out as bbc_oracle_count.
+ */
+typedef struct { uint32_t stamp, b1, b2, pad; } sbucket;
+
+typedef struct {
+  const og_graph* g;
+  int side;
+  int64_t n;
+  const uint32_t* lst; /* per centre: prank << 1 | neg, ascending */
+  int64_t next, chunk;
+  pthread_mutex_t lock;
+} sjob;
+
+typedef struct { sjob* j; u128 bal, unb; uint64_t admitted, scanned; int err; } sworker_arg;
+
+static void* sworker(void* p) {
+  sworker_arg* wa = (sworker_arg*)p;
+  sjob* j = wa->j;
+  const og_graph* g = j->g;
+  const int64_t *off_s = j->side ? g->off_v : g->off_u, *off_o = j->side ? g->off_u : g->off_v;
+  const int32_t* adj_s = j->side ? g->adj_v : g->adj_u;
+  const int8_t* sgn_s = j->side ? g->sgn_v : g->sgn_u;
+  const int64_t* prank = j->side ? g->prank_v : g->prank_u;
+  int64_t n = j->n;
+  sbucket* b = (sbucket*)calloc((size_t)n + 1, sizeof(sbucket));
+  uint32_t* touched = (uint32_t*)malloc(((size_t)n + 1) * 4);
+  if (!b || !touched) { wa->err = E_NOMEM; free(b); free(touched); return NULL; }
+  u128 bal = 0, unb = 0;
+  uint64_t admitted = 0, scanned = 0;
+  for (;;) {
+    pthread_mutex_lock(&j->lock);
+    int64_t lo = j->next;
+    j->next += j->chunk;
+    pthread_mutex_unlock(&j->lock);
+    if (lo >= n) break;
+    int64_t hi = lo + j->chunk < n ? lo + j->chunk : n;
+    for (int64_t a = lo; a < hi; ++a) {
+      uint32_t st = (uint32_t)a + 1, pu = (uint32_t)prank[a];
+      int64_t nt = 0;
+      for (int64_t e = off_s[a]; e < off_s[a + 1]; ++e) {
+        const uint32_t* l = j->lst + off_o[adj_s[e]];
+        uint32_t neg = sgn_s[e] < 0;
+        int64_t f = 0;
+        for (;; ++f) {
+          uint32_t x = l[f], r = x >> 1;
+          if (r >= pu) break; /* u itself is in the list: the scan always stops */
+          sbucket* q = &b[r];
+          if (q->stamp != st) { q->stamp = st; q->b1 = 0; q->b2 = 0; touched[nt++] = r; }
+          if ((x & 1) == neg) q->b1++; else q->b2++;
+        }
+        admitted += (uint64_t)f;
+        scanned += (uint64_t)f + 1;
+      }
+      uint64_t sb = 0, su = 0;
+      for (int64_t t = 0; t < nt; ++t) {
+        uint64_t c1 = b[touched[t]].b1, c2 = b[touched[t]].b2;
+        sb += c1 * (c1 - (c1 > 0)) / 2 + c2 * (c2 - (c2 > 0)) / 2;
+        su += c1 * c2;
+      }
+      bal += sb; unb += su; /* per anchor < 2^64: sum over w of deg(u)^2 */
+    }
+  }
+  free(b); free(touched);
+  wa->bal = bal; wa->unb = unb; wa->admitted = admitted; wa->scanned = scanned;
+  return NULL;
+}
+
+int bbc_oracle_count_sorted(const og_graph* g, int side, int threads, uint64_t* out) {
+  if (side < 0) side = g->n_u <= g->n_v ? 0 : 1;
+  if (threads < 1 || side > 1) return E_ARG;
+  int64_t n = side ? g->n_v : g->n_u, no = side ? g->n_u : g->n_v;
+  const int64_t *off_s = side ? g->off_v : g->off_u, *off_o = side ? g->off_u : g->off_v;
+  const int32_t* adj_s = side ? g->adj_v : g->adj_u;
+  const int8_t* sgn_s = side ? g->sgn_v : g->sgn_u;
+  const int64_t* prank = side ? g->prank_v : g->prank_u;
+  /* centre lists in ascending anchor rank: append anchors in rank order */
+  uint32_t* lst = (uint32_t*)malloc(((size_t)g->m + 1) * 4);
+  int64_t* cur = (int64_t*)malloc(((size_t)no + 1) * 8);
+  int64_t* inv = (int64_t*)malloc(((size_t)n + 1) * 8);
+  if (!lst || !cur || !inv) { free(lst); free(cur); free(inv); return E_NOMEM; }
+  memcpy(cur, off_o, ((size_t)no + 1) * 8);
+  for (int64_t a = 0; a < n; ++a) inv[prank[a]] = a;
+  for (int64_t r = 0; r < n; ++r) {
+    int64_t a = inv[r];
+    for (int64_t e = off_s[a]; e < off_s[a + 1]; ++e)
+      lst[cur[adj_s[e]]++] = (uint32_t)r << 1 | (uint32_t)(sgn_s[e] < 0);
+  }
+  free(cur); free(inv);
+  sjob j;
+  memset(&j, 0, sizeof(j));
+  j.g = g; j.side = side; j.n = n; j.lst = lst;
+  pthread_mutex_init(&j.lock, NULL);
+  j.chunk = n / ((int64_t)threads * 256);
+  if (j.chunk < 1) j.chunk = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+  sworker_arg* wa = (sworker_arg*)calloc((size_t)threads, sizeof(sworker_arg));
+  for (int t = 0; t < threads; ++t) wa[t].j = &j;
+  for (int t = 1; t < threads; ++t) pthread_create(&th[t], NULL, sworker, &wa[t]);
+  sworker(&wa[0]);
+  for (int t = 1; t < threads; ++t) pthread_join(th[t], NULL);
+  u128 bal = 0, unb = 0;
+  uint64_t adm = 0, scn = 0;
+  int err = OK;
+  for (int t = 0; t < threads; ++t) {
+    bal += wa[t].bal; unb += wa[t].unb; adm += wa[t].admitted; scn += wa[t].scanned;
+    if (wa[t].err) err = wa[t].err;
+  }
+  free(th); free(wa); free(lst);
+  pthread_mutex_destroy(&j.lock);
+  out[0] = (uint64_t)bal; out[1] = (uint64_t)(bal >> 64);
+  out[2] = (uint64_t)unb; out[3] = (uint64_t)(unb >> 64);
+  out[4] = adm; out[5] = scn; out[6] = (uint64_t)side;
+  if (err) return err;
+  return (out[1] || out[3]) ? E_OVERFLOW : OK;
+}
+
 int64_t bbc_oracle_graph_info(const og_graph* g, int what) {
   switch (what) {
     case 0: return g->n_u;

@@ -49,6 +49,8 @@ def _load():
         L.bbc_oracle_count.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int64, P]
         L.bbc_oracle_graph_free.argtypes = [P]
         L.bbc_oracle_graph_free.restype = None
+        L.bbc_oracle_count_sorted.restype = ctypes.c_int
+        L.bbc_oracle_count_sorted.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
         L.bbc_oracle_count_2k.restype = ctypes.c_int
         L.bbc_oracle_count_2k.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P]
         L.bbc_oracle_classify.restype = ctypes.c_int
@@ -95,6 +97,16 @@ class OracleGraph:
             threads = len(os.sched_getaffinity(0))
         out = (ctypes.c_uint64 * 8)()
         rc = _load().bbc_oracle_count(self._h, side, threads, stride, out)
+        if rc not in (0, E_OVERFLOW):
+            raise OracleError(rc, 0)
+        return OracleResult(balanced=int(out[0]) | (int(out[1]) << 64), unbalanced=int(out[2]) | (int(out[3]) << 64),
+                            admitted=int(out[4]), scanned=int(out[5]), side=int(out[6]))
+
+    def count_sorted(self, side: int = -1, threads: int | None = None) -> OracleResult:
+        """The reference's sort_neighbors traversal (buckets.py:87-111, early exit at the
+        anchor's rank): same counts, scanned = admitted + one stop per record."""
+        out = (ctypes.c_uint64 * 8)()
+        rc = _load().bbc_oracle_count_sorted(self._h, side, threads or len(os.sched_getaffinity(0)), out)
         if rc not in (0, E_OVERFLOW):
             raise OracleError(rc, 0)
         return OracleResult(balanced=int(out[0]) | (int(out[1]) << 64), unbalanced=int(out[2]) | (int(out[3]) << 64),

@@ -58,7 +58,7 @@ def build_libbbc(force: bool = False) -> Path:
             if p.wait():
                 raise subprocess.CalledProcessError(p.returncode, cmd)
         tmp = LIBBBC.with_suffix(".so.tmp")
-        _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)])
+        _run([NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-ldl"])
         os.replace(tmp, LIBBBC)
     return LIBBBC
 

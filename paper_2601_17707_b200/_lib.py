@@ -33,7 +33,8 @@ EXPORTED_SYMBOLS = (
     "bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work", "bbc_task_order",
     "bbc_round_counters", "bbc_classify", "bbc_count_2k", "bbc_ingest_text", "bbc_ingest_edges",
     "bbc_ingest_graph", "bbc_ingest_destroy", "bbc_graph_info", "bbc_graph_stream", "bbc_graph_destroy", "bbc_device_count", "bbc_last_error",
-    "bbc_last_error_info",
+    "bbc_last_error_info", "bbc_multi_create", "bbc_multi_count", "bbc_multi_devices", "bbc_multi_graph",
+    "bbc_multi_destroy", "bbc_count_multi",
 )
 
 
@@ -91,12 +92,23 @@ def load() -> ctypes.CDLL:
         L.bbc_graph_stream.restype = P
         L.bbc_graph_destroy.argtypes = [P]
         L.bbc_graph_destroy.restype = None
+        L.bbc_multi_create.argtypes = [I32, ctypes.POINTER(ctypes.c_int32), I64, I64, I64, P, P, P, I32,
+                                       ctypes.POINTER(P)]
+        L.bbc_multi_count.argtypes = [P, ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
+        L.bbc_multi_devices.argtypes = [P, ctypes.POINTER(ctypes.c_int32), I32]
+        L.bbc_multi_graph.argtypes = [P, I32]
+        L.bbc_multi_graph.restype = P
+        L.bbc_multi_destroy.argtypes = [P]
+        L.bbc_multi_destroy.restype = None
+        L.bbc_count_multi.argtypes = [I32, ctypes.POINTER(ctypes.c_int32), I64, I64, I64, P, P, P, I32,
+                                      ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
         L.bbc_device_count.argtypes = []
         L.bbc_last_error.restype = ctypes.c_char_p
         L.bbc_last_error_info.restype = ctypes.c_int64
         for name in ("bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work",
                      "bbc_task_order", "bbc_round_counters", "bbc_classify", "bbc_count_2k", "bbc_graph_info",
-                     "bbc_device_count", "bbc_ingest_text", "bbc_ingest_edges", "bbc_ingest_graph"):
+                     "bbc_device_count", "bbc_ingest_text", "bbc_ingest_edges", "bbc_ingest_graph",
+                     "bbc_multi_create", "bbc_multi_count", "bbc_multi_devices", "bbc_count_multi"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
         return L
@@ -140,11 +152,26 @@ class CountResult:
     count_ms: float
 
 
-class DeviceGraph:
-    """Owning handle of one device-resident graph (bbc_graph*)."""
+def _result(out, st: Stats) -> CountResult:
+    return CountResult(balanced=int(out[0]) | (int(st.balanced_hi) << 64),
+                       unbalanced=int(out[1]) | (int(st.unbalanced_hi) << 64), wedges=int(st.wedges),
+                       wedges_total=int(st.wedges_total), w_u=int(st.w_u), w_v=int(st.w_v),
+                       anchor_side=int(st.anchor_side), blocks=int(st.blocks), threads=int(st.threads),
+                       tile_span=int(st.tile_span), tasks=int(st.tasks), preprocess_ms=float(st.preprocess_ms),
+                       count_ms=float(st.count_ms))
 
-    def __init__(self, handle: int, device: int):
+
+class DeviceGraph:
+    """Owning handle of one device-resident graph (bbc_graph*).
+
+    A handle is not re-entrant (include/bbc.h): its accumulators, queue and per-CTA work
+    buffer are reused by every call, so calls on one handle are serialised by a lock
+    (ctypes releases the GIL during them)."""
+
+    def __init__(self, handle: int, device: int, owned: bool = True):
         self._h = ctypes.c_void_p(handle)
+        self._owned = owned
+        self._lock = threading.Lock()
         self.device = device
         info = (ctypes.c_int64 * 8)()
         load().bbc_graph_info(self._h, info, 8)
@@ -182,15 +209,11 @@ class DeviceGraph:
                  part_count=part_count, flags=flags)
         out = (ctypes.c_uint64 * 2)()
         st = Stats()
-        rc = load().bbc_count(self._h, ctypes.byref(o), out, ctypes.byref(st))
+        with self._lock:
+            rc = load().bbc_count(self._h, ctypes.byref(o), out, ctypes.byref(st))
         if rc and rc != 3:
             _raise(rc)
-        return CountResult(balanced=int(out[0]) | (int(st.balanced_hi) << 64),
-                           unbalanced=int(out[1]) | (int(st.unbalanced_hi) << 64), wedges=int(st.wedges),
-                           wedges_total=int(st.wedges_total), w_u=int(st.w_u), w_v=int(st.w_v),
-                           anchor_side=int(st.anchor_side), blocks=int(st.blocks), threads=int(st.threads),
-                           tile_span=int(st.tile_span), tasks=int(st.tasks), preprocess_ms=float(st.preprocess_ms),
-                           count_ms=float(st.count_ms))
+        return _result(out, st)
 
     CLASS_NAMES = ("coherent_pp_pp", "coherent_pp_mm", "coherent_mm_mm", "incoherent_pm_pm", "mixed_pp_pm",
                    "mixed_pm_mm")
@@ -203,7 +226,8 @@ class DeviceGraph:
         o = Opts(algo=algo, blocks=blocks, part_index=part_index, part_count=part_count, flags=flags)
         out = (ctypes.c_uint64 * 12)()
         st = Stats()
-        rc = load().bbc_classify(self._h, ctypes.byref(o), out, ctypes.byref(st))
+        with self._lock:
+            rc = load().bbc_classify(self._h, ctypes.byref(o), out, ctypes.byref(st))
         if rc:
             _raise(rc)
         return ({n: int(out[2 * i]) | (int(out[2 * i + 1]) << 64) for i, n in enumerate(self.CLASS_NAMES)},
@@ -218,14 +242,16 @@ class DeviceGraph:
         o = Opts(algo=algo, blocks=blocks, part_index=part_index, part_count=part_count, flags=flags)
         out = (ctypes.c_uint64 * 2)()
         st = Stats()
-        rc = load().bbc_count_2k(self._h, k, ctypes.byref(o), out, ctypes.byref(st))
+        with self._lock:
+            rc = load().bbc_count_2k(self._h, k, ctypes.byref(o), out, ctypes.byref(st))
         if rc and rc != 3:
             _raise(rc)
         return int(out[0]) | (int(out[1]) << 64), rc == 3, float(st.count_ms)
 
     def block_work(self, n: int) -> list[int]:
         buf = (ctypes.c_uint64 * max(n, 1))()
-        rc = load().bbc_block_work(self._h, buf, n)
+        with self._lock:
+            rc = load().bbc_block_work(self._h, buf, n)
         if rc:
             _raise(rc)
         return [int(buf[i]) for i in range(n)]
@@ -244,8 +270,9 @@ class DeviceGraph:
         n = self.n_anchors
         ids = np.empty(max(n, 1), dtype=np.int32)
         work = np.empty(max(n, 1), dtype=np.uint64)
-        rc = load().bbc_task_order(self._h, algo, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                                   work.ctypes.data, n)
+        with self._lock:
+            rc = load().bbc_task_order(self._h, algo, ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                       work.ctypes.data, n)
         if rc:
             _raise(rc)
         return ids[:n], work[:n]
@@ -254,9 +281,61 @@ class DeviceGraph:
         return int(load().bbc_graph_stream(self._h) or 0)
 
     def close(self) -> None:
-        if self._h is not None and self._h.value:
-            load().bbc_graph_destroy(self._h)
-        self._h = None
+        with self._lock:
+            if self._h is not None and self._h.value and self._owned:
+                load().bbc_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class MultiGraph:
+    """Owning handle of a graph replicated on several GPUs of this process (bbc_multi*):
+    sharded upload + NCCL all-gather + replicated build; counts are start-vertex
+    partitions summed by one NCCL all-reduce (include/bbc.h, bbc_multi_*)."""
+
+    def __init__(self, n_u: int, n_v: int, u: np.ndarray, v: np.ndarray, s: np.ndarray, devices: list[int],
+                 side_rule: int = SIDE_CHEAPER):
+        u = np.ascontiguousarray(u, dtype=np.int32)
+        v = np.ascontiguousarray(v, dtype=np.int32)
+        s = np.ascontiguousarray(s, dtype=np.int8)
+        devs = (ctypes.c_int32 * len(devices))(*devices)
+        h = ctypes.c_void_p()
+        rc = load().bbc_multi_create(len(devices), devs, n_u, n_v, len(u), u.ctypes.data, v.ctypes.data,
+                                     s.ctypes.data, side_rule, ctypes.byref(h))
+        if rc:
+            _raise(rc)
+        self._h = h
+        self._lock = threading.Lock()
+        self.devices = list(devices)
+        self.replicas = [DeviceGraph(load().bbc_multi_graph(h, i), d, owned=False) for i, d in enumerate(devices)]
+        r0 = self.replicas[0]
+        self.n_u, self.n_v, self.m, self.anchor_side, self.n_anchors, self.w_s, self.w_u, self.w_v = (
+            r0.n_u, r0.n_v, r0.m, r0.anchor_side, r0.n_anchors, r0.w_s, r0.w_u, r0.w_v)
+
+    def count(self, algo: int = ALGO_GBBCPP, tile_span: int = 0, blocks: int = 0, flags: int = 0) -> CountResult:
+        if self._h is None:
+            raise DeviceError("multi-GPU handle already closed")
+        o = Opts(algo=algo, tile_span=tile_span, blocks=blocks, flags=flags)
+        out = (ctypes.c_uint64 * 2)()
+        st = Stats()
+        with self._lock:
+            rc = load().bbc_multi_count(self._h, ctypes.byref(o), out, ctypes.byref(st))
+        if rc and rc != 3:
+            _raise(rc)
+        return _result(out, st)
+
+    def close(self) -> None:
+        with self._lock:
+            for r in getattr(self, "replicas", []):
+                r._h = None
+            if self._h is not None and self._h.value:
+                load().bbc_multi_destroy(self._h)
+            self._h = None
 
     def __del__(self):
         try:

@@ -655,6 +655,11 @@ int create_common(int device, int64_t n_u, int64_t n_v, int64_t m, const int32_t
 
 }  // namespace
 
+int create_graph(int device, int64_t n_u, int64_t n_v, int64_t m, const int32_t* u, const int32_t* v,
+                 const int8_t* s, int32_t side_rule, bool host, bbc_graph** out) {
+  return create_common(device, n_u, n_v, m, u, v, s, side_rule, host, out);
+}
+
 void destroy_graph(Graph& g) {
   if (g.stream) {
     cudaSetDevice(g.device);

@@ -19,7 +19,9 @@ per (graph, device, side rule) and cached on the immutable graph object.
 
 Mapping of the reference's parallelism knobs onto the device:
   * ``workers`` (fork-pool size) -> number of GPUs in this process, clamped to the
-    visible devices; start vertices are partitioned and the exact sums added;
+    visible devices; the edge list is uploaded in shards and all-gathered over NVLink,
+    every GPU builds the CSR, counts its start-vertex partition, and the exact sums are
+    added by one NCCL all-reduce (``bbc_multi_*``, csrc/bbc_multi.cu);
   * ``TileConfig.tile_size`` -> end-vertex tile span of the shared-memory counters,
     ``TileConfig.block_count`` -> CTAs of the static G-BBC grid;
   * ``block_count`` of the dynamic engine -> persistent CTAs claiming from the global
@@ -184,30 +186,27 @@ def _devices(n: int) -> list[int]:
     return list(range(min(max(n, 1), avail)))
 
 
+def multi_graph(g: SignedBipartiteGraph, devices: list[int], side: Side | None = None) -> _lib.MultiGraph:
+    """The graph replicated on ``devices`` (sharded upload + NCCL all-gather + replicated
+    build, csrc/bbc_multi.cu), built on first use and cached on the graph."""
+    key = ("multi", tuple(devices), side)
+    mg = g._device_cache.get(key)
+    if mg is None:
+        u, v, s = g.edge_arrays()
+        mg = _lib.MultiGraph(g.u_count, g.v_count, u, v, s, devices, _SIDE_RULE[side])
+        g._device_cache[key] = mg
+    return mg
+
+
 def _count(g: SignedBipartiteGraph, devices: list[int], algo: int, side: Side | None = None, tile_span: int = 0,
            blocks: int = 0) -> tuple[int, int, list[_lib.CountResult]]:
-    """Exact (balanced, unbalanced) over start-vertex partitions, one per device."""
-    graphs = [device_graph(g, d, side) for d in devices]
-    if len(graphs) == 1:
-        r = graphs[0].count(algo, tile_span, blocks)
-        return r.balanced, r.unbalanced, [r]
-    results: list = [None] * len(graphs)
-    errors: list = []
-
-    def run(i: int) -> None:
-        try:
-            results[i] = graphs[i].count(algo, tile_span, blocks, part_index=i, part_count=len(graphs))
-        except BaseException as e:  # re-raised on the caller's thread
-            errors.append(e)
-
-    threads = [threading.Thread(target=run, args=(i,)) for i in range(len(graphs))]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
-    if errors:
-        raise errors[0]
-    return sum(r.balanced for r in results), sum(r.unbalanced for r in results), results
+    """Exact (balanced, unbalanced): one device, or start-vertex partitions over several
+    GPUs summed by one NCCL all-reduce inside libbbc (bbc_multi_count)."""
+    if len(devices) == 1:
+        r = device_graph(g, devices[0], side).count(algo, tile_span, blocks)
+    else:
+        r = multi_graph(g, devices, side).count(algo, tile_span, blocks)
+    return r.balanced, r.unbalanced, [r]
 
 
 def _checked(balanced: int) -> int:
