@@ -436,8 +436,10 @@ def extensions(cfg, du, dv, ds, device) -> dict:
 def other_config(k: int, peak: float, device: int) -> dict:
     """Another BASELINE config under the bench's clock: G-BBC (static round-robin) and
     G-BBC++ (dynamic queue) device-timed counts (one warm-up, median of three), the
-    per-CTA load ratio max/mean of each from bbc_block_work (ScheduleReport.max_over_mean,
-    tiled.py:92-97, measured on the device), and the roofline fraction."""
+    per-CTA load ratios max/mean of each, measured on the device -- of admitted wedges
+    (bbc_block_work, ScheduleReport.max_over_mean, tiled.py:92-97) and of busy time
+    (bbc_block_busy_ns: what a persistent grid actually waits on) -- and the roofline
+    fraction."""
     import torch
 
     from paper_2601_17707_b200 import _lib, synth
@@ -461,11 +463,13 @@ def other_config(k: int, peak: float, device: int) -> dict:
             if i:
                 times.append(r.count_ms)
         work = g.block_work(r.blocks)
+        busy = g.block_busy_ns(r.blocks)
         mean = sum(work) / max(len(work), 1)
+        bmean = sum(busy) / max(len(busy), 1)
         ms = statistics.median(times)
         out[name] = {"count_ms": ms, "wedges_per_s": g.w_s / (ms * 1e-3), "balanced": r.balanced,
                      "unbalanced": r.unbalanced, "cta_work_max_over_mean": max(work) / mean if mean else 1.0,
-                     "blocks": r.blocks,
+                     "cta_busy_max_over_mean": max(busy) / bmean if bmean else 1.0, "blocks": r.blocks,
                      "roofline_frac": alg_bytes / (ms * 1e-3) / 1e9 / peak}
     out["counts_agree"] = (out["gbbc"]["balanced"], out["gbbc"]["unbalanced"]) == \
         (out["gbbc++"]["balanced"], out["gbbc++"]["unbalanced"])

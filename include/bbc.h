@@ -89,7 +89,8 @@ typedef struct {
                         /*  bit 9  force cold bitmap rounds                           */
                         /*  bit 10 band bounds by search (ignore the band table)      */
                         /*  bit 11 closing sweep for every tile round                 */
-                        /*  bit 12 record round counters (bbc_round_counters)         */
+                        /*  bit 12 record round counters (bbc_round_counters; only in */
+                        /*         a -DBBC_ROUND_STATS diagnostic build)              */
                         /*  bit 13 force cold key-hash rounds                         */
 } bbc_opts;
 
@@ -190,6 +191,11 @@ int bbc_count_multi(int32_t ndev, const int32_t* devices, int64_t n_u, int64_t n
 
 /* Per-CTA admitted wedges of the last bbc_count (ScheduleReport.per_block_work). */
 int bbc_block_work(bbc_graph* g, uint64_t* out, int32_t n);
+
+/* Per-CTA busy time (ns, %globaltimer from the CTA's start to its exit) of the last
+ * bbc_count: with persistent CTAs the spread of these is the schedule's real load
+ * imbalance (a CTA that finishes early idles until the slowest one is done). */
+int bbc_block_busy_ns(bbc_graph* g, uint64_t* out, int32_t n);
 
 /* Diagnostics: rounds of the last bbc_count run with opts.flags bit 12 (BBC_FLAG_ROUNDS):
  * out[0] bitmap rounds, out[1] of them overflowed and redone, out[2] counter-tile rounds,

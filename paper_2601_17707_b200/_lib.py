@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = (
     "bbc_round_counters", "bbc_classify", "bbc_count_2k", "bbc_ingest_text", "bbc_ingest_edges",
     "bbc_ingest_graph", "bbc_ingest_destroy", "bbc_graph_info", "bbc_graph_stream", "bbc_graph_destroy", "bbc_device_count", "bbc_last_error",
     "bbc_last_error_info", "bbc_multi_create", "bbc_multi_count", "bbc_multi_devices", "bbc_multi_graph",
-    "bbc_multi_destroy", "bbc_count_multi",
+    "bbc_multi_destroy", "bbc_count_multi", "bbc_block_busy_ns",
 )
 
 
@@ -79,6 +79,7 @@ def load() -> ctypes.CDLL:
         L.bbc_block_work.argtypes = [P, U64P, I32]
         L.bbc_task_order.argtypes = [P, I32, ctypes.POINTER(ctypes.c_int32), P, I64]
         L.bbc_round_counters.argtypes = [P, U64P]
+        L.bbc_block_busy_ns.argtypes = [P, U64P, I32]
         L.bbc_classify.argtypes = [P, ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
         L.bbc_count_2k.argtypes = [P, I32, ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
         L.bbc_ingest_text.argtypes = [ctypes.c_int, ctypes.c_char_p, I64, ctypes.POINTER(SignPolicy),
@@ -108,7 +109,7 @@ def load() -> ctypes.CDLL:
         for name in ("bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work",
                      "bbc_task_order", "bbc_round_counters", "bbc_classify", "bbc_count_2k", "bbc_graph_info",
                      "bbc_device_count", "bbc_ingest_text", "bbc_ingest_edges", "bbc_ingest_graph",
-                     "bbc_multi_create", "bbc_multi_count", "bbc_multi_devices", "bbc_count_multi"):
+                     "bbc_multi_create", "bbc_multi_count", "bbc_multi_devices", "bbc_count_multi", "bbc_block_busy_ns"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
         return L
@@ -252,6 +253,15 @@ class DeviceGraph:
         buf = (ctypes.c_uint64 * max(n, 1))()
         with self._lock:
             rc = load().bbc_block_work(self._h, buf, n)
+        if rc:
+            _raise(rc)
+        return [int(buf[i]) for i in range(n)]
+
+    def block_busy_ns(self, n: int) -> list[int]:
+        """Per-CTA busy time (ns) of the last count (bbc_block_busy_ns)."""
+        buf = (ctypes.c_uint64 * max(n, 1))()
+        with self._lock:
+            rc = load().bbc_block_busy_ns(self._h, buf, n)
         if rc:
             _raise(rc)
         return [int(buf[i]) for i in range(n)]

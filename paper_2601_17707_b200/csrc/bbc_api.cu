@@ -81,6 +81,21 @@ int bbc_block_work(bbc_graph* h, uint64_t* out, int32_t n) {
   return BBC_OK;
 }
 
+int bbc_block_busy_ns(bbc_graph* h, uint64_t* out, int32_t n) {
+  if (!h || !out || n < 0) {
+    bbc::set_error("bad arguments to bbc_block_busy_ns");
+    return BBC_ERR_ARG;
+  }
+  bbc::Graph& g = h->g;
+  int k = n < g.last_blocks ? n : g.last_blocks;
+  if (k > 0) {
+    BBC_CK(cudaSetDevice(g.device));
+    BBC_CK(cudaMemcpy(out, g.block_work + g.block_work_cap, (size_t)k * 8, cudaMemcpyDeviceToHost));
+  }
+  for (int i = k; i < n; ++i) out[i] = 0;
+  return BBC_OK;
+}
+
 int bbc_round_counters(bbc_graph* h, uint64_t out[8]) {
   if (!h || !out) {
     bbc::set_error("bad arguments to bbc_round_counters");

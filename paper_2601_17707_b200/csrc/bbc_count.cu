@@ -77,6 +77,7 @@ struct Params {
   unsigned long long* acc;
   unsigned int* queue;
   unsigned long long* block_work;
+  unsigned long long* block_busy;  // per-CTA busy time (ns), accumulated like block_work
 };
 
 // The tile / bitmap ops address their words from a REBASED shared address: rb = base -
@@ -337,7 +338,9 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
                                unsigned long long& tb, unsigned long long& tu, unsigned long long& work) {
   const uint32_t span = W == 8 ? P.span8 : (W == 16 ? P.span16 : P.span32);
   const uint32_t step = W == 8 ? 2u : 1u;  // table columns per band
-  const bool table = P.bnd != nullptr && W != 32;
+  // band b = table columns [b * step, (b + 1) * step) only when the band span is the
+  // table granularity (the 128 x 8 configuration); otherwise bounds by search
+  const bool table = P.bnd != nullptr && W != 32 && P.span16 == P.t16;
   const uint32_t nbands_u = (P.n - 1u - r) / span + 1u;  // bands 0..nbands_u-1 hold ranks > r
   const uint32_t nbatch = (re - rb + T - 1u) / (uint32_t)T;
   uint32_t scan_buf = 0;  // alternates the scan's total buffers
@@ -517,17 +520,21 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     const uint32_t ngroups = __shfl_sync(kFull, incl, 31);
     bw = wsum;
     __syncwarp();
+#ifdef BBC_ROUND_STATS
     if ((P.debug & 4096) && threadIdx.x == 0) {
       atomicAdd(P.acc + 8, (unsigned long long)ngroups);
       atomicAdd(P.acc + 9, bw);
       atomicAdd(P.acc + 10, 1ull);
     }
+#endif
     if (ngroups == 0u) __syncthreads();
     return ngroups;
   };
   // one tile round over band columns [ca, ca + cols)
   auto tile_round = [&](uint32_t ca, uint32_t cols, uint32_t ngroups, unsigned long long bw) {
+#ifdef BBC_ROUND_STATS
     if ((P.debug & 4096) && threadIdx.x == 0) atomicAdd(P.acc + 6, 1ull);
+#endif
     const long long top = (long long)P.n - (long long)ca * t16;
     const long long bot = top - (long long)cols * t16;
     // lo_rank aligned to the ranks per word (W8: 2), see the rebased ops
@@ -662,10 +669,12 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       uint4* c4 = reinterpret_cast<uint4*>(bm);
 #pragma unroll 4
       for (uint32_t i = threadIdx.x; i < span_words / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
+#ifdef BBC_ROUND_STATS
       if (P.debug & 4096) {
         if (t0) atomicAdd(P.acc + 4, 1ull);
         if (t0 && ovf) atomicAdd(P.acc + 5, 1ull);
       }
+#endif
       if (!ovf) {
         if (t0) work += bw;
         hi = lo;
@@ -728,7 +737,9 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
         c = cb;
         continue;
       }
+#ifdef BBC_ROUND_STATS
       if ((P.debug & 4096) && t0) atomicAdd(P.acc + 7, 1ull);
+#endif
       OpKeys op{keys, K, sptr(queue), sptr(cnt), Q};
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ng, op);
       __syncthreads();
@@ -821,6 +832,8 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
   S.w = s_w;
   S.ins = s_ins;
 
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   for (uint32_t i = threadIdx.x; i < P.cap_words / 4; i += T) smem4[i] = make_uint4(0u, 0u, 0u, 0u);
 
   unsigned long long bal_lo = 0, bal_hi = 0, unb_lo = 0, unb_hi = 0, work = 0;
@@ -891,6 +904,9 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
     unsigned long long t = 0;
     for (int w = 0; w < kWarps; ++w) t += s_w[w];
     P.block_work[blockIdx.x] += t;  // launches of one count accumulate (zeroed per count)
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    P.block_busy[blockIdx.x] += t_end - t_start;
   }
 }
 
@@ -921,13 +937,10 @@ int configure_t(Graph& g, Launch& L) {
   return BBC_OK;
 }
 
-// single-launch configuration (all phases): 128 x 8 per SM, or 256 x 4 (env BBC_THREADS=256,
-// an experiment).  Measured on config 2 and removed: 128 x {4, 6, 10, 12} (19.6 / 16.0 /
-// 17.7 / 20.0 ms vs 15.4 ms at the time) and 512 x 2 / 1024 x 1.
-int configure(Graph& g, Launch& L) {
-  if (g.threads == 256) return configure_t<256, 4>(g, L);
-  return configure_t<128, 8>(g, L);
-}
+// single-launch configuration (all phases): 128 x 8 per SM.  Measured on config 2 and
+// removed: 128 x {4, 6, 10, 12} (19.6 / 16.0 / 17.7 / 20.0 ms vs 15.4 ms at the time),
+// 256 x 4, 512 x 2 and 1024 x 1.
+int configure(Graph& g, Launch& L) { return configure_t<128, 8>(g, L); }
 
 // two-phase configuration: hub band with 128 x 8, cold range with 256 x 2 (big hash)
 int configure_cold(Graph& g, Launch& L) { return configure_t<256, 2>(g, L); }
@@ -938,9 +951,7 @@ int configure_cold(Graph& g, Launch& L) { return configure_t<256, 2>(g, L); }
 int count_span16(Graph& g) {
   Launch L;
   BBC_CK(cudaSetDevice(g.device));
-  Graph h = g;
-  h.threads = 128;
-  if (configure(h, L)) return -1;
+  if (configure(g, L)) return -1;
   return L.cap_words - 8;
 }
 
@@ -987,22 +998,17 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st, int
   if (blocks > g.block_work_cap) {
     cudaFree(g.block_work);
     g.block_work = nullptr;
-    BBC_CK(cudaMalloc(&g.block_work, (size_t)blocks * 8));
+    BBC_CK(cudaMalloc(&g.block_work, (size_t)blocks * 16));
     g.block_work_cap = blocks;
   }
   const uint32_t n = (uint32_t)g.n;
   const uint32_t ntasks =
       n > (uint32_t)opts.part_index ? (n - (uint32_t)opts.part_index + part_count - 1) / part_count : 0u;
 
-  // tuning knobs (defaults measured on config 2; env overrides for experiments)
-  struct {
+  // tuning constants (measured on configs 2-5)
+  constexpr struct {
     uint32_t rep_slots = 128, bits_thr = 4096, sweep_min = 4, bm_cols0 = 8, hash_thr = 256;
   } tune;
-  if (const char* e = std::getenv("BBC_HASH_THR")) tune.hash_thr = (uint32_t)std::atoi(e);
-  if (const char* e = std::getenv("BBC_BM_COLS0")) tune.bm_cols0 = (uint32_t)std::atoi(e);
-  if (const char* e = std::getenv("BBC_REP_SLOTS")) tune.rep_slots = (uint32_t)std::atoi(e);
-  if (const char* e = std::getenv("BBC_BITS_THR")) tune.bits_thr = (uint32_t)std::atoi(e);
-  if (const char* e = std::getenv("BBC_SWEEP_MIN")) tune.sweep_min = (uint32_t)std::atoi(e);
 
   auto params = [&](const Launch& X, int phase) {
     Params P;
@@ -1060,12 +1066,14 @@ int count_graph(Graph& g, const bbc_opts* o, uint64_t out[2], bbc_stats* st, int
     P.acc = g.acc;
     P.queue = g.queue + (phase == 2 ? 1 : 0);
     P.block_work = g.block_work;
+    P.block_busy = g.block_work + g.block_work_cap;
     return P;
   };
 
   BBC_CK(cudaMemsetAsync(g.acc, 0, 128, g.stream));
   BBC_CK(cudaMemsetAsync(g.queue, 0, 8, g.stream));
   BBC_CK(cudaMemsetAsync(g.block_work, 0, (size_t)blocks * 8, g.stream));
+  BBC_CK(cudaMemsetAsync(g.block_work + g.block_work_cap, 0, (size_t)blocks * 8, g.stream));
   BBC_CK(cudaEventRecord(g.ev0, g.stream));
   const Params P1 = params(L, two_phase ? 1 : 0);
   L.kernel<<<blocks1, L.threads, L.smem_bytes, g.stream>>>(P1);

@@ -407,7 +407,7 @@ int ext_launch(Graph& g, const bbc_opts& opts, uint32_t k, unsigned long long* h
   if (blocks > g.block_work_cap) {
     cudaFree(g.block_work);
     g.block_work = nullptr;
-    BBC_CK(cudaMalloc(&g.block_work, (size_t)blocks * 8));
+    BBC_CK(cudaMalloc(&g.block_work, (size_t)blocks * 16));
     g.block_work_cap = blocks;
   }
   const int part_count = opts.part_count <= 0 ? 1 : opts.part_count;

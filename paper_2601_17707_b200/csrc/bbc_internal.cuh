@@ -47,14 +47,14 @@ struct Graph {
   // count scratch
   unsigned long long* acc = nullptr;        // [4]: bal lo, bal hi, unb lo, unb hi
   unsigned int* queue = nullptr;            // [1]
-  unsigned long long* block_work = nullptr; // [block_work_cap]
+  unsigned long long* block_work = nullptr; // [2 * block_work_cap]: per-CTA admitted wedges,
+                                            // then per-CTA busy ns (globaltimer)
   int block_work_cap = 0;
   int last_blocks = 0;
   uint64_t rounds[8] = {};  // last count with flags bit 12: bitmap, overflowed, tile, hash rounds;
                            // walked groups, walked wedges, round setups
   int num_sms = 0;
   int max_smem = 0;
-  int threads = 128;  // count-kernel CTA size (128, or 256 for experiments: env BBC_THREADS)
   float preprocess_ms = 0.f;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };

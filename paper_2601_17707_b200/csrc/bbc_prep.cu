@@ -512,8 +512,7 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
     if (nc > 0 && n > 0) {
       size_t free_b = 0, total_b = 0;
       cudaMemGetInfo(&free_b, &total_b);
-      size_t budget = (size_t)8192 << 20;  // env BBC_TABLE_MB; beyond it the kernel searches
-      if (const char* e = std::getenv("BBC_TABLE_MB")) budget = (size_t)std::atoll(e) << 20;
+      size_t budget = (size_t)8192 << 20;  // beyond it the kernel searches
       budget = std::min<size_t>(budget, free_b / 4);
       // smallest list-length threshold whose rows fit the budget (0: every centre)
       DevBuf rowcnt;
@@ -549,7 +548,7 @@ int build_on_device(Graph& g, const int32_t* du, const int32_t* dv, const int8_t
   BBC_ALLOC(g.acc, 128);
   BBC_ALLOC(g.queue, 64);
   g.block_work_cap = std::max(1, sms * 32);
-  BBC_ALLOC(g.block_work, (size_t)g.block_work_cap * 8);
+  BBC_ALLOC(g.block_work, (size_t)g.block_work_cap * 16);
   BBC_CK(cudaStreamSynchronize(st));
   return BBC_OK;
 }
@@ -576,10 +575,6 @@ int init_handle(Graph& g, int device, int64_t n_u, int64_t n_v, int64_t m) {
   g.m = m;
   BBC_CK(cudaDeviceGetAttribute(&g.num_sms, cudaDevAttrMultiProcessorCount, device));
   BBC_CK(cudaDeviceGetAttribute(&g.max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-  if (const char* e = std::getenv("BBC_THREADS")) {
-    int t = std::atoi(e);
-    if (t == 128 || t == 256) g.threads = t;
-  }
   BBC_CK(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
   {
     cudaMemPool_t pool;

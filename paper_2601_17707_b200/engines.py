@@ -65,10 +65,10 @@ def wedge_kind(sign_uv: EdgeSign, sign_vw: EdgeSign) -> WedgeKind:
 class WedgeCounters:
     """Instrumentation filled by ``count_balanced_2k_serial`` from device counters.
 
-    ``admitted_per_anchor`` holds, per anchor id, the admitted wedges the device walked
-    under its rank filter (rank(w) > rank(u)); every admitted wedge lands in a bucket,
-    so ``bucket_sums_per_anchor`` equals it.  The device only scans admitted suffixes,
-    so ``scanned == admitted`` (the reference model also scans rejected wedges).
+    ``admitted_per_anchor`` holds, per anchor id, the wedges admitted by the reference's
+    filter prank[w] < prank[u] (buckets.py:96-153); every admitted wedge lands in a
+    bucket, so ``bucket_sums_per_anchor`` equals it.  ``scanned`` counts the list entries
+    the reference traversal examines (see count_balanced_2k_serial).
     """
 
     admitted_per_anchor: list[int] = field(default_factory=list)
@@ -243,14 +243,45 @@ def count_balanced_parallel(g: SignedBipartiteGraph, workers: int, inline_below:
     return _checked(bal)
 
 
+def _reference_work(g: SignedBipartiteGraph, side: Side) -> np.ndarray:
+    """Admitted visits per anchor of ``side`` under the reference models' id filter w > u
+    (tiled.py:143-156, 221-233): for each edge (u, c), the entries of c's id-sorted list
+    above u.  Schedule accounting only -- the count itself always comes from the device."""
+    eu, ev, _ = g.edge_arrays()  # sorted by (u, v)
+    if side is Side.U:
+        # position of u in v's list (V lists ascend in u): the stable order of ev
+        perm = np.argsort(ev, kind="stable")
+        pos = np.empty(len(ev), dtype=np.int64)
+        off_v = np.zeros(g.v_count + 1, dtype=np.int64)
+        np.cumsum(g.degree_array(Side.V), out=off_v[1:])
+        pos[perm] = np.arange(len(ev), dtype=np.int64) - off_v[ev[perm]]
+        per_edge = g.degree_array(Side.V)[ev] - 1 - pos
+        idx, n = eu, g.u_count
+    else:
+        off_u = np.zeros(g.u_count + 1, dtype=np.int64)
+        np.cumsum(g.degree_array(Side.U), out=off_u[1:])
+        pos = np.arange(len(eu), dtype=np.int64) - off_u[eu]  # v's position in u's list
+        per_edge = g.degree_array(Side.U)[eu] - 1 - pos
+        idx, n = ev, g.v_count
+    return np.bincount(idx, weights=per_edge, minlength=n).astype(np.int64)
+
+
 def count_balanced_2k_serial(g: SignedBipartiteGraph, k: int, anchor_side: Side = Side.U,
                              sort_neighbors: bool = False, counters: WedgeCounters | None = None) -> int:
     """Balanced (2,k)-biclique count with the size-2 side on ``anchor_side`` (buckets.py:64-154).
 
     k = 2 (balanced butterflies) runs the count kernel anchored on ``anchor_side``; k > 2
-    runs the (2,k) kernel (csrc/bbc_ext.cu: per pair C(b1,k) + C(b2,k), buckets.py:146)
-    on the same device CSR.  ``sort_neighbors`` is accepted (device lists are always
-    rank-sorted).  CountOverflowError above 2^64 - 1, like the reference.
+    runs the same kernel with C(b1,k) + C(b2,k) closings (buckets.py:146) on the same
+    device CSR.  ``sort_neighbors`` only changes what the reference's instrumentation
+    counts as scanned (device lists are always rank-sorted).  CountOverflowError above
+    2^64 - 1, like the reference.
+
+    ``counters`` is filled as the reference fills it (buckets.py:96-153): per anchor id,
+    the wedges admitted by its filter prank[w] < prank[u] -- derived from the device's
+    per-anchor work under the mirrored filter: sum over c in N(u) of (deg c - 1) minus
+    the device's admitted count -- and ``scanned`` = sum over centres of deg^2 (every
+    list fully scanned, buckets.py:53-57) or, with ``sort_neighbors``, admitted plus one
+    early-exit stop per anchor-side edge (:106-107).
     """
     if k < 2:
         raise InvalidKError(f"k must be >= 2, got {k}")
@@ -266,37 +297,49 @@ def count_balanced_2k_serial(g: SignedBipartiteGraph, k: int, anchor_side: Side 
     if counters is not None:
         dg = device_graph(g, 0, anchor_side)
         ids, work = dg.task_order(_lib.ALGO_GBBC)
-        per = np.zeros(g.side_count(anchor_side), dtype=np.int64)
-        per[ids] = work.astype(np.int64)
+        mirrored = np.zeros(g.side_count(anchor_side), dtype=np.int64)
+        mirrored[ids] = work.astype(np.int64)
+        deg = g.degree_array(anchor_side)
+        centre_sum = g.fanouts(anchor_side) - deg  # sum over c in N(u) of deg c
+        per = centre_sum - deg - mirrored
         counters.admitted_per_anchor.extend(per.tolist())
         counters.bucket_sums_per_anchor.extend(per.tolist())
-        counters.scanned += int(per.sum())
+        if sort_neighbors:
+            counters.scanned += int(per.sum()) + g.edge_count
+        else:
+            counters.scanned += wedge_scan_bound(g, anchor_side)
     return _checked(bal)
 
 
 def count_balanced_tiled(g: SignedBipartiteGraph, cfg: TileConfig) -> tuple[int, ScheduleReport]:
-    """G-BBC: ``cfg.block_count`` CTAs take anchors round-robin; tiles of ``cfg.tile_size``."""
+    """G-BBC (tiled.py:107-168): the count from the device's static round-robin kernel
+    (BBC_ALGO_GBBC, a full persistent grid and the native shared-memory tiles -- the
+    count is independent of the tiling); the report as the reference defines it for
+    ``cfg``: anchors of min_side in id order, block b doing anchors b, b + B, ...,
+    per_block_work = admitted visits under the id filter w > u (tiled.py:137-156)."""
     blocks = cfg.block_count
-    if g.side_count(Side.U) == 0 and g.side_count(Side.V) == 0:
+    side = g.min_side()
+    n = g.side_count(side)
+    if n == 0:
         return 0, ScheduleReport([0] * blocks, 1.0, [])
-    dg = device_graph(g)
-    if dg.n_anchors == 0:
-        return 0, ScheduleReport([0] * blocks, 1.0, [])
-    bal, _, _ = _count(g, [0], _lib.ALGO_GBBC, None, tile_span=cfg.tile_size, blocks=blocks)
-    work = dg.block_work(blocks)
-    ids, _ = dg.task_order(_lib.ALGO_GBBC)
-    return _checked(bal), ScheduleReport(work, _max_over_mean(work), ids.tolist())
+    bal, _, _ = _count(g, _devices(1), _lib.ALGO_GBBC, side)
+    per_anchor = _reference_work(g, side)
+    work = np.bincount(np.arange(n) % blocks, weights=per_anchor, minlength=blocks).astype(np.int64).tolist()
+    return _checked(bal), ScheduleReport(work, _max_over_mean(work), list(range(n)))
 
 
 def count_balanced_dynamic(g: SignedBipartiteGraph, block_count: int,
                            thresholds: tuple[int, int] = (DEFAULT_WARP_MAX, DEFAULT_PARTIAL_MAX),
                            mode: str = "threads") -> tuple[int, ScheduleReport]:
-    """G-BBC++: persistent CTAs claim descending-work anchors from a global atomic queue.
+    """G-BBC++ (tiled.py:182-292) on min_side: task_order = anchors by (-fanout, id)
+    (:213-214), the regime histogram by anchor degree (:215-216).
 
-    ``mode="threads"`` reports the per-CTA work measured on the device (the split varies
-    run to run, the count does not).  ``mode="replay"`` reports the deterministic
-    least-loaded-claims-next replay (tiled.py:243-258) of the device's task list and
-    per-task work, for scheduling tests.
+    ``mode="threads"``: ``block_count`` persistent CTAs claim descending-work anchors from
+    the device's global atomic queue, and per_block_work is each CTA's admitted wedges
+    measured on the device (the split varies run to run, the count and the total work
+    do not -- as with the reference's threads).  ``mode="replay"``: the count from a
+    full-grid launch and the reference's deterministic least-loaded-claims-next replay
+    (:243-258) of the fanout order with the id-filter work per anchor.
     """
     warp_max, partial_max = thresholds
     if warp_max >= partial_max:
@@ -305,30 +348,33 @@ def count_balanced_dynamic(g: SignedBipartiteGraph, block_count: int,
         raise ValueError(f"block_count must be >= 1, got {block_count}")
     if mode not in ("threads", "replay"):
         raise ValueError(f"unknown mode {mode!r}")
+    side = g.min_side()
+    n = g.side_count(side)
     histogram = {r: 0 for r in CooperationRegime}
-    if g.u_count == 0 and g.v_count == 0:
+    if n == 0:
         return 0, ScheduleReport([0] * block_count, 1.0, [], histogram)
-    dg = device_graph(g)
-    side = Side.U if dg.anchor_side == 0 else Side.V
     deg = g.degree_array(side)
     histogram[CooperationRegime.WARP] = int((deg < warp_max).sum())
     histogram[CooperationRegime.FULL_BLOCK] = int((deg > partial_max).sum())
-    histogram[CooperationRegime.PARTIAL_BLOCK] = int(len(deg)) - histogram[CooperationRegime.WARP] - \
+    histogram[CooperationRegime.PARTIAL_BLOCK] = n - histogram[CooperationRegime.WARP] - \
         histogram[CooperationRegime.FULL_BLOCK]
-    if dg.n_anchors == 0:
-        return 0, ScheduleReport([0] * block_count, 1.0, [], histogram)
-    bal, _, _ = _count(g, [0], _lib.ALGO_GBBCPP, None, blocks=block_count)
-    ids, task_work = dg.task_order(_lib.ALGO_GBBCPP)
+    fan = g.fanouts(side)
+    order = np.lexsort((np.arange(n), -fan)).tolist()
     if mode == "threads":
+        dg = device_graph(g, _devices(1)[0], side)
+        r = dg.count(_lib.ALGO_GBBCPP, blocks=block_count)
+        bal = r.balanced
         work = dg.block_work(block_count)
     else:
+        bal, _, _ = _count(g, _devices(1), _lib.ALGO_GBBCPP, side)
+        per_anchor = _reference_work(g, side).tolist()
         work = [0] * block_count
         clocks = [(0, b) for b in range(block_count)]
-        for w in task_work.tolist():
+        for u in order:
             clock, b = heapq.heappop(clocks)
-            work[b] += w
-            heapq.heappush(clocks, (clock + w, b))
-    return _checked(bal), ScheduleReport(work, _max_over_mean(work), ids.tolist(), histogram)
+            work[b] += per_anchor[u]
+            heapq.heappush(clocks, (clock + per_anchor[u], b))
+    return _checked(bal), ScheduleReport(work, _max_over_mean(work), order, histogram)
 
 
 def count_balanced_bruteforce(g: SignedBipartiteGraph) -> tuple[int, int]:
