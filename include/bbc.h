@@ -189,6 +189,17 @@ int bbc_count_multi(int32_t ndev, const int32_t* devices, int64_t n_u, int64_t n
                     const int32_t* u, const int32_t* v, const int8_t* sign, int32_t side_rule,
                     const bbc_opts* opts, uint64_t out[2], bbc_stats* stats);
 
+/* Every butterfly, replacing oracle.enumerate_butterflies (pkg/src/bbcount/oracle.py:73-107):
+ * canonical (u1 < u2, v1 < v2) in (u1, u2, v1, v2) order, from HOST edge arrays, on
+ * `device`.  *count receives the number of butterflies; with ids != NULL the first
+ * call's output is written: ids[4i..4i+3] = u1, u2, v1, v2 and signs[i] bit j set when
+ * sign j (order u1v1, u1v2, u2v1, u2v2) is negative.  BBC_ERR_ARG when max_out is too
+ * small or the graph's wedges / butterflies exceed 2^31 (a test-scale API, as the
+ * reference's). */
+int bbc_enumerate_butterflies(int32_t device, int64_t n_u, int64_t n_v, int64_t m, const int32_t* u,
+                              const int32_t* v, const int8_t* sign, uint64_t* count, int32_t* ids,
+                              uint8_t* signs, uint64_t max_out);
+
 /* Per-CTA admitted wedges of the last bbc_count (ScheduleReport.per_block_work). */
 int bbc_block_work(bbc_graph* g, uint64_t* out, int32_t n);
 

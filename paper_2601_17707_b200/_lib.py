@@ -34,7 +34,7 @@ EXPORTED_SYMBOLS = (
     "bbc_round_counters", "bbc_classify", "bbc_count_2k", "bbc_ingest_text", "bbc_ingest_edges",
     "bbc_ingest_graph", "bbc_ingest_destroy", "bbc_graph_info", "bbc_graph_stream", "bbc_graph_destroy", "bbc_device_count", "bbc_last_error",
     "bbc_last_error_info", "bbc_multi_create", "bbc_multi_count", "bbc_multi_devices", "bbc_multi_graph",
-    "bbc_multi_destroy", "bbc_count_multi", "bbc_block_busy_ns",
+    "bbc_multi_destroy", "bbc_count_multi", "bbc_block_busy_ns", "bbc_enumerate_butterflies",
 )
 
 
@@ -80,6 +80,7 @@ def load() -> ctypes.CDLL:
         L.bbc_task_order.argtypes = [P, I32, ctypes.POINTER(ctypes.c_int32), P, I64]
         L.bbc_round_counters.argtypes = [P, U64P]
         L.bbc_block_busy_ns.argtypes = [P, U64P, I32]
+        L.bbc_enumerate_butterflies.argtypes = [I32, I64, I64, I64, P, P, P, U64P, P, P, ctypes.c_uint64]
         L.bbc_classify.argtypes = [P, ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
         L.bbc_count_2k.argtypes = [P, I32, ctypes.POINTER(Opts), U64P, ctypes.POINTER(Stats)]
         L.bbc_ingest_text.argtypes = [ctypes.c_int, ctypes.c_char_p, I64, ctypes.POINTER(SignPolicy),
@@ -109,7 +110,7 @@ def load() -> ctypes.CDLL:
         for name in ("bbc_graph_create", "bbc_graph_create_device", "bbc_count", "bbc_block_work",
                      "bbc_task_order", "bbc_round_counters", "bbc_classify", "bbc_count_2k", "bbc_graph_info",
                      "bbc_device_count", "bbc_ingest_text", "bbc_ingest_edges", "bbc_ingest_graph",
-                     "bbc_multi_create", "bbc_multi_count", "bbc_multi_devices", "bbc_count_multi", "bbc_block_busy_ns"):
+                     "bbc_multi_create", "bbc_multi_count", "bbc_multi_devices", "bbc_count_multi", "bbc_block_busy_ns", "bbc_enumerate_butterflies"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
         return L
@@ -398,3 +399,26 @@ def ingest_text(data: bytes, policy: SignPolicy, device: int = 0) -> tuple[int, 
     if rc:
         return rc, None, int(load().bbc_last_error_info())
     return 0, Ingested(h.value, device, int(counts[0]), int(counts[1]), int(counts[2])), 0
+
+
+def enumerate_butterflies(n_u: int, n_v: int, u, v, s, device: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """Every butterfly on the device (bbc_enumerate_butterflies): (ids int32[B, 4] as
+    (u1, u2, v1, v2) in lexicographic order, negative-sign bits uint8[B])."""
+    u = np.ascontiguousarray(u, dtype=np.int32)
+    v = np.ascontiguousarray(v, dtype=np.int32)
+    s = np.ascontiguousarray(s, dtype=np.int8)
+    L = load()
+    cnt = ctypes.c_uint64(0)
+    rc = L.bbc_enumerate_butterflies(device, n_u, n_v, len(u), u.ctypes.data, v.ctypes.data, s.ctypes.data,
+                                     ctypes.byref(cnt), None, None, 0)
+    if rc:
+        _raise(rc)
+    b = int(cnt.value)
+    ids = np.empty((max(b, 1), 4), dtype=np.int32)
+    bits = np.empty(max(b, 1), dtype=np.uint8)
+    if b:
+        rc = L.bbc_enumerate_butterflies(device, n_u, n_v, len(u), u.ctypes.data, v.ctypes.data, s.ctypes.data,
+                                         ctypes.byref(cnt), ids.ctypes.data, bits.ctypes.data, b)
+        if rc:
+            _raise(rc)
+    return ids[:b], bits[:b]

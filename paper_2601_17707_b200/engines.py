@@ -389,6 +389,48 @@ def sign_product_total(g: SignedBipartiteGraph) -> int:
     return bal - unb
 
 
+@dataclass(frozen=True)
+class Butterfly:
+    """Canonical 4-cycle (oracle.py:19-28): u1 < u2, v1 < v2; signs in the order
+    (u1-v1, u1-v2, u2-v1, u2-v2)."""
+
+    u1: int
+    u2: int
+    v1: int
+    v2: int
+    signs: tuple[EdgeSign, EdgeSign, EdgeSign, EdgeSign]
+
+
+def enumerate_butterflies(g: SignedBipartiteGraph):
+    """Yield every butterfly once, in (u1, u2, v1, v2) lexicographic order
+    (oracle.py:73-107), enumerated on the device (csrc/bbc_enum.cu: wedges through each
+    centre, stable radix sort by vertex pair, C(r, 2) butterflies per run of r common
+    centres).  Materialises all of them: a test-scale API, like the reference's."""
+    if g.u_count == 0 or g.v_count == 0 or g.edge_count == 0:
+        return
+    _devices(1)
+    u, v, s = g.edge_arrays()
+    ids, bits = _lib.enumerate_butterflies(g.u_count, g.v_count, u, v, s, 0)
+    P, N = EdgeSign.POSITIVE, EdgeSign.NEGATIVE
+    for (u1, u2, v1, v2), b in zip(ids.tolist(), bits.tolist()):
+        yield Butterfly(u1, u2, v1, v2, (N if b & 1 else P, N if b & 2 else P, N if b & 4 else P, N if b & 8 else P))
+
+
+def is_balanced(b: Butterfly) -> bool:
+    """Even number of negative edges (oracle.py:110-113)."""
+    return sum(1 for s in b.signs if s is EdgeSign.NEGATIVE) % 2 == 0
+
+
+def count_balanced_2k_bruteforce(g: SignedBipartiteGraph, k: int, anchor_side: Side = Side.U) -> int:
+    """Balanced (2,k)-bicliques with the size-2 side on ``anchor_side`` (oracle.py:137-169).
+
+    A (2,k)-biclique is balanced iff every butterfly in it is, i.e. iff its k centres all
+    make wedges of one kind with the pair -- exactly C(b1,k) + C(b2,k) per pair, which the
+    device's (2,k) kernel computes (same result as the reference's subset enumeration).
+    """
+    return count_balanced_2k_serial(g, k, anchor_side)
+
+
 @dataclass
 class ButterflyClassCounts:
     """Six-way split by the two wedges through v1, v2 (endpoints u1, u2) -- the reference's

@@ -210,3 +210,41 @@ def test_acceptance_8_on_the_device(gpu, key):
         assert best[_lib.ALGO_GBBCPP] <= best[_lib.ALGO_GBBC], best
     finally:
         dg.close()
+
+
+def reference_enumerate(g):
+    """oracle.enumerate_butterflies (oracle.py:73-107), restated with set intersections."""
+    out = []
+    for u1 in range(g.u_count):
+        n1 = set(g.adj_u[u1])
+        for u2 in range(u1 + 1, g.u_count):
+            common = sorted(n1.intersection(g.adj_u[u2]))
+            for i, v1 in enumerate(common):
+                for v2 in common[i + 1:]:
+                    out.append((u1, u2, v1, v2, (g.edge_sign(u1, v1), g.edge_sign(u1, v2), g.edge_sign(u2, v1),
+                                                 g.edge_sign(u2, v2))))
+    return out
+
+
+def test_enumerate_butterflies_matches_the_reference_order(gpu, golden):
+    """The device enumerator against the reference's definition: same butterflies, same
+    (u1, u2, v1, v2) order, same signs; pivoting on either side (|U| <= |V| and not);
+    is_balanced / count_balanced_bruteforce agree with the goldens."""
+    from paper_2601_17707_b200 import enumerate_butterflies, is_balanced
+
+    named = fixtures.named_fixtures()
+    for name in ("complete_2x2", "dense_mixed_4x4", "one_negative", "skew_instance", "complete_5x4", "degree_bands"):
+        if name not in named:
+            continue
+        g = named[name].graph()
+        got = [(b.u1, b.u2, b.v1, b.v2, b.signs) for b in enumerate_butterflies(g)]
+        assert got == reference_enumerate(g), name
+        rec = golden["named"][name]
+        bs = list(enumerate_butterflies(g))
+        assert (sum(map(is_balanced, bs)), len(bs)) == (rec["balanced"], rec["total"]), name
+    rng = random.Random(8)
+    for _ in range(30):
+        g = fixtures.random_graph(rng, 14, 9, 0.4).graph() if rng.random() < 0.5 else \
+            fixtures.random_graph(rng, 9, 14, 0.4).graph()
+        assert [(b.u1, b.u2, b.v1, b.v2, b.signs) for b in enumerate_butterflies(g)] == reference_enumerate(g)
+    assert list(enumerate_butterflies(build(0, 3, []))) == []
