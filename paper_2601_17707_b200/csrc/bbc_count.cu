@@ -135,7 +135,17 @@ struct OpTileClose {
   }
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int j) {
     const uint32_t v = w ^ sg;
-    if (W == 8) {
+    if (W == 8 && !KG) {
+      // the increment selects this wedge's own byte; a byte dot product (IDP4A) of the old
+      // word with it adds the own count, with the end vertex's other byte the other count
+      const uint32_t hs = (w & 1u) << 4;
+      const uint32_t inc = 1u << (hs | ((v >> 28) & 8u));
+      const uint32_t a = rb + ((w << 1) & 0xfffffffcu);
+      const uint32_t old = s_atom_add(a, inc);
+      b32 = __dp4a(old, inc, b32);
+      u32 = __dp4a(old, (0x101u << hs) ^ inc, u32);
+      if (KEEP) touched[j] = a;
+    } else if (W == 8) {
       const uint32_t sh = ((w & 1u) << 4) | ((v >> 28) & 8u);
       const uint32_t a = rb + ((w << 1) & 0xfffffffcu);
       const uint32_t old = s_atom_add(a, 1u << sh);
@@ -237,13 +247,14 @@ struct OpBits {
       bits[j] = ok ? (((w >> 15) & 0x10000u) ^ sgs1) << (w & 15u) : 0u;
       old[j] = s_atom_or(ok ? rb + ((w >> 2) & 0x0ffffffcu) : dummy, bits[j]);
     }
-    uint32_t rep = 0;
+    // one LOP3 per wedge: any seen bit that was already set (a repeat) shows in `any`
+    uint32_t any = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) rep |= ((old[j] & bits[j] & 0xffffu) != 0u ? 1u : 0u) << j;
-    if (rep) {
+    for (int j = 0; j < 8; ++j) any |= old[j] & bits[j];
+    if (any & 0xffffu) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (!((rep >> j) & 1u)) continue;
+        if (!(old[j] & bits[j] & 0xffffu)) continue;
         // counted as negative only if it is negative and the parity bit was already set
         const uint32_t cneg = ((old[j] & bits[j]) >> 16) != 0u;
         const uint32_t idx = s_atom_add(count, 1u);
@@ -387,7 +398,7 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
       unsigned long long bw;
       const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w, scan_buf++);
       if ((int)threadIdx.x < nb) S.pfx[threadIdx.x] = ex;
-      __syncthreads();
+      block_sync();
       work += myw;
       band_w += bw;
       // the closing of a band is chosen once, from its first batch: the sweep when the band
@@ -410,7 +421,7 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
           walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
         }
       }
-      __syncthreads();  // the next batch overwrites the record arrays
+      block_sync();  // the next batch overwrites the record arrays
     }
     if (band_w > 0) {
       if (mode == kDense) {
@@ -420,7 +431,7 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
 #pragma unroll 4
         for (uint32_t i = threadIdx.x; i < (band_words + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
       }
-      __syncthreads();
+      block_sync();
     }
   }
 }
@@ -486,7 +497,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       S.lo[threadIdx.x] = lo | (recx & 0x80000000u);
       S.hi[threadIdx.x] = hi;
     }
-    __syncthreads();
+    block_sync();
     constexpr int R = T / 32;
     const int lane = threadIdx.x & 31;
     uint32_t ng[R], run = 0;
@@ -527,7 +538,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       atomicAdd(P.acc + 10, 1ull);
     }
 #endif
-    if (ngroups == 0u) __syncthreads();
+    if (ngroups == 0u) block_sync();
     return ngroups;
   };
   // one tile round over band columns [ca, ca + cols)
@@ -549,7 +560,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
 #pragma unroll
       for (int j = 0; j < 8; ++j) op.touched[j] = 0xffffffffu;
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
-      __syncthreads();
+      block_sync();
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (op.touched[j] != 0xffffffffu) s_st(op.touched[j], 0u);
@@ -558,14 +569,14 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       // closing sweep costs ~9 instructions per counter word, inline closing ~4 per wedge)
       OpTileClose<W, false, KG> op{base, &tb, &tu, P.k};
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
-      __syncthreads();
+      block_sync();
       uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
       for (uint32_t i = threadIdx.x; i < (band_words + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
     } else {
       // dense rounds: no-return increments and the shared-memory closing sweep
       OpTileDense<W> op{base};
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
-      __syncthreads();
+      block_sync();
       sweep<T, W, KG>(S.cnt, band_words, tb, tu, P.k);
     }
     // no trailing barrier: every caller's next tile use comes after a setup (two barriers)
@@ -612,7 +623,9 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       const uint32_t cb = min(c + cols, ncols);
       const uint32_t lo = col(cb, hi);
       uint32_t* cnt = S.ins + (parity++ & 1u);
-      if (t0) *cnt = 0u;  // its last reader finished before the previous round's barriers
+      // reset and read of the repeat counter are volatile: the walk increments it through
+      // inline-asm atomics the compiler cannot see
+      if (t0) *(volatile uint32_t*)cnt = 0u;  // its last reader finished before the previous round's barriers
       unsigned long long bw;
       const uint32_t ng = setup(hi, lo, bw);
       if (ng == 0u) {
@@ -633,8 +646,8 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       uint32_t* vals = keys + K;
       OpBits op{sptr(bm) - ((lo_rank >> 4) << 2), sptr(queue), sptr(cnt), Q, sptr(bm) + ((threadIdx.x & 31u) << 2)};
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ng, op);
-      __syncthreads();
-      const uint32_t nq = *cnt;
+      block_sync();
+      const uint32_t nq = *(volatile const uint32_t*)cnt;
       const bool ovf = nq > Q;
       if (nq != 0u && !ovf) {
         // count the repeats per end vertex; the inserting entry becomes the closer and
@@ -648,7 +661,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
           const uint32_t neg = (bm[rel >> 4] >> (16u + (rel & 15u))) & 1u;
           queue[i] = (h >> 31) ? (h | (neg << 30)) : 0u;
         }
-        __syncthreads();
+        block_sync();
         // close every repeated end vertex (first wedge from the parity bit + the counts)
         for (uint32_t i = threadIdx.x; i < nq; i += T) {
           const uint32_t e = queue[i];
@@ -716,7 +729,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       const uint32_t cb = min(c + cols, ncols);
       const uint32_t lo = col(cb, hi);
       uint32_t* cnt = S.ins + (parity++ & 1u);
-      if (t0) *cnt = 0u;
+      if (t0) *(volatile uint32_t*)cnt = 0u;
       unsigned long long bw;
       const uint32_t ng = setup(hi, lo, bw);
       if (ng == 0u) {
@@ -727,7 +740,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       }
       if (bw > target && cols > 1u) {  // too many wedges for the hash: narrower, no walk
         cols = max(1u, min(cols / 2u, (uint32_t)((unsigned long long)cols * target / bw)));
-        __syncthreads();  // every warp is done with this set-up's record arrays
+        block_sync();  // every warp is done with this set-up's record arrays
         continue;
       }
       if (bw > target) {  // a single column denser than the hash: one counter-tile round
@@ -742,8 +755,8 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
 #endif
       OpKeys op{keys, K, sptr(queue), sptr(cnt), Q};
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ng, op);
-      __syncthreads();
-      const uint32_t nq = *cnt;
+      block_sync();
+      const uint32_t nq = *(volatile const uint32_t*)cnt;
       const bool ovf = nq > Q;
       if (nq != 0u && !ovf) {
         // count the repeats per key slot in the secondary set; the entry that inserted the
@@ -754,7 +767,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
           atomicAdd(&svals[r & 0x7fffffffu], (e >> 31) ? 0x10000u : 1u);
           queue[i] = (r >> 31) ? ((r & 0x3fffffffu) | 0x80000000u | ((keys[h] >> 31) << 30)) : 0u;
         }
-        __syncthreads();
+        block_sync();
         for (uint32_t i = threadIdx.x; i < nq; i += T) {
           const uint32_t e = queue[i];
           if (e == 0u) continue;
@@ -839,11 +852,11 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
   unsigned long long bal_lo = 0, bal_hi = 0, unb_lo = 0, unb_hi = 0, work = 0;
   uint32_t next = blockIdx.x;
   if (threadIdx.x == 0) s_task = P.dynamic ? atomicAdd(P.queue, 1u) : next;
-  __syncthreads();
+  block_sync();
   for (;;) {
     const uint32_t t = s_task;
     next += gridDim.x;
-    __syncthreads();  // every thread holds t before s_task is overwritten
+    block_sync();  // every thread holds t before s_task is overwritten
     if (t >= P.ntasks) break;
     // claim the following task now so the queue round trip overlaps this anchor
     if (threadIdx.x == 0) s_task = P.dynamic ? atomicAdd(P.queue, 1u) : next;
@@ -851,7 +864,7 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
     const uint32_t r = P.dynamic ? P.order[gidx] : gidx;
     const unsigned long long w_a = P.awork[r];
     if (w_a == 0ull) {
-      __syncthreads();  // publish the claimed task
+      block_sync();  // publish the claimed task
       continue;
     }
     const uint32_t rb = P.aoff[r], re = P.aoff[r + 1];
@@ -861,7 +874,7 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
     // a count so that phases agree on which anchors they split
     const bool fast = P.fast && deg <= min((uint32_t)T, P.fast_max);
     if (!fast && P.phase == 2) {  // general-path anchors are done entirely in phase 1
-      __syncthreads();
+      block_sync();
       continue;
     }
     if (fast && deg <= 255u)
@@ -876,7 +889,7 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
       process_anchor<T, 32, KG>(P, S, r, rb, re, tb, tu, work);
     add128(bal_lo, bal_hi, tb);
     add128(unb_lo, unb_hi, tu);
-    __syncthreads();  // publish the claimed task
+    block_sync();  // publish the claimed task
   }
 
   // exact 128-bit reduction: warp shuffle, then one pair of global atomics per warp
@@ -899,7 +912,7 @@ __global__ void __launch_bounds__(T, MINB) k_count(Params P) {
     atomicAdd(&P.acc[3], unb_hi + (old + unb_lo < old ? 1ull : 0ull));
     s_w[threadIdx.x >> 5] = work;
   }
-  __syncthreads();
+  block_sync();
   if (threadIdx.x == 0) {
     unsigned long long t = 0;
     for (int w = 0; w < kWarps; ++w) t += s_w[w];

@@ -230,7 +230,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
       unsigned long long bw;
       const uint32_t ex = scan_sum<T>(ng, myw, ngroups, bw, S.v, S.w, scan_buf++);
       if ((int)threadIdx.x < nb) S.pfx[threadIdx.x] = ex;
-      __syncthreads();
+      block_sync();
       if (hashing && b > 0 && bw > target && nbw > 1u) {  // too many wedges: narrower, no walk
         width = max(1u, min(nbw / 2u, (uint32_t)((unsigned long long)nbw * target / bw)));
         redo = true;
@@ -254,7 +254,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
           part[5] += op.c5;
         }
         if (2ull * bw < target) width = min(2u * width, nbands);
-        __syncthreads();
+        block_sync();
         break;
       }
       if (dense < 0) dense = wide || bw * nbatch >= 2ull * band_words;
@@ -277,10 +277,10 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
           walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
         }
       }
-      __syncthreads();  // the next batch overwrites the record arrays
+      block_sync();  // the next batch overwrites the record arrays
     }
     if (redo) {
-      __syncthreads();  // every warp is done with this set-up's record arrays
+      block_sync();  // every warp is done with this set-up's record arrays
       continue;
     }
     b += nbw;
@@ -289,7 +289,7 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
     if (hashed) {
 #pragma unroll 4
       for (uint32_t i = threadIdx.x; i < K / 2u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
-      __syncthreads();
+      block_sync();
       continue;
     }
     const uint32_t nq = (band_words + 3u) / 4u;
@@ -318,11 +318,11 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
           part[5] += bb * d;
         }
       }
-      __syncthreads();
+      block_sync();
     }
 #pragma unroll 4
     for (uint32_t i = threadIdx.x; i < nq; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
-    __syncthreads();
+    block_sync();
   }
   for (int i = 0; i < 6; ++i) add128(acc[2 * i], acc[2 * i + 1], part[i]);
 }
@@ -349,17 +349,17 @@ __global__ void __launch_bounds__(T, MINB) k_ext(ExtParams P) {
   uint32_t ovf = 0;
   uint32_t next = blockIdx.x;
   if (threadIdx.x == 0) s_task = P.dynamic ? atomicAdd(P.queue, 1u) : next;
-  __syncthreads();
+  block_sync();
   for (;;) {
     const uint32_t t = s_task;
     next += gridDim.x;
-    __syncthreads();
+    block_sync();
     if (t >= P.ntasks) break;
     if (threadIdx.x == 0) s_task = P.dynamic ? atomicAdd(P.queue, 1u) : next;
     const uint32_t gidx = P.part_index + t * P.part_count;
     const uint32_t r = P.dynamic ? P.order[gidx] : gidx;
     if (P.awork[r] != 0ull) ext_anchor<T, MODE>(P, S, r, P.aoff[r], P.aoff[r + 1], acc, ovf, work);
-    __syncthreads();
+    block_sync();
   }
   // exact reduction: warp shuffle of the 128-bit values, one pair of atomics per warp
   const int lane = threadIdx.x & 31;
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(T, MINB) k_ext(ExtParams P) {
   for (int o = 16; o; o >>= 1) work += __shfl_xor_sync(kFull, work, o);
   if (ovf) atomicOr(&s_ovf, 1u);
   if (lane == 0) s_w[threadIdx.x >> 5] = work;
-  __syncthreads();
+  block_sync();
   if (threadIdx.x == 0) {
     unsigned long long tw = 0;
     for (int w = 0; w < T / 32; ++w) tw += s_w[w];

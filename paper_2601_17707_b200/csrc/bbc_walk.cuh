@@ -9,6 +9,15 @@ namespace bbc {
 
 constexpr uint32_t kFull = 0xffffffffu;
 
+// Block barrier for code whose warps may reach it diverged.  __syncthreads() is bar.sync,
+// i.e. barrier.sync.aligned, which requires every warp to arrive converged; the count
+// kernel's warps are routinely split by data-dependent loops (galloping record searches,
+// per-lane queue loops) when they reach a barrier, and on config 4 (1 B edges) that broke
+// the CTA's barrier pairing (warps walking one round while others set up the next: wrong
+// bounds, out-of-range shared-memory atomics; compute-sanitizer synccheck reported
+// "divergent thread(s) in warp").  The non-aligned form counts arrivals per thread.
+__device__ __forceinline__ void block_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
+
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -72,7 +81,7 @@ __device__ __forceinline__ uint32_t scan_sum(uint32_t v, unsigned long long w, u
   unsigned long long* sw = s_w + (buf & 1u) * 32u;
   if (lane == 31) sv[warp] = x;
   if (lane == 0) sw[warp] = w;
-  __syncthreads();
+  block_sync();
   uint32_t a = lane < kWarps ? sv[lane] : 0u;
   unsigned long long bsum = lane < kWarps ? sw[lane] : 0ull;
 #pragma unroll
