@@ -49,7 +49,7 @@ def parse_args():
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extensions", action="store_true", help="skip the 8(f) classification / (2,k) timings")
-    p.add_argument("--ext-configs", default="3,5",
+    p.add_argument("--ext-configs", default="3,5,4",
                    help="other BASELINE configs timed in `extensions` (G-BBC vs G-BBC++, roofline); '' = none")
     p.add_argument("--launcher-selftest", action="store_true",
                    help="spawn/rendezvous check only (gloo, no GPU): rank 0 prints one JSON line")
