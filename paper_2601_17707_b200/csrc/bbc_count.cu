@@ -91,6 +91,17 @@ struct OpTileDense {
   uint32_t rb;
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
     const uint32_t v = w ^ sg;  // bit 31: parity (1 = negative wedge)
+#ifdef BBC_MATCH
+    // north_star (2) match aggregation (experiment): lanes incrementing the same
+    // counter byte combine, the lowest one adds the group's size
+    if (W == 8) {
+      const uint32_t sh = ((w & 1u) << 4) | ((v >> 28) & 8u);
+      const uint32_t a = rb + ((w << 1) & 0xfffffffcu);
+      const uint32_t peers = __match_any_sync(__activemask(), (a << 3) | (sh >> 3));
+      if ((threadIdx.x & 31u) == (uint32_t)(__ffs(peers) - 1)) s_red_add(a, (uint32_t)__popc(peers) << sh);
+      return;
+    }
+#endif
     if (W == 8)
       s_red_add(rb + ((w << 1) & 0xfffffffcu), 1u << (((w & 1u) << 4) | ((v >> 28) & 8u)));
     else
@@ -135,6 +146,26 @@ struct OpTileClose {
   }
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int j) {
     const uint32_t v = w ^ sg;
+#ifdef BBC_MATCH
+    if (W == 8 && !KG) {
+      // match aggregation (experiment): a group of g lanes adding to one counter byte that
+      // held c adds c + (c+1) + ... + (c+g-1) = g*c + g(g-1)/2 to the own sum and g times
+      // the other byte to the other sum -- exactly the sum of the g single increments
+      const uint32_t hs = (w & 1u) << 4;
+      const uint32_t sh = hs | ((v >> 28) & 8u);
+      const uint32_t a = rb + ((w << 1) & 0xfffffffcu);
+      const uint32_t peers = __match_any_sync(__activemask(), (a << 3) | (sh >> 3));
+      if ((threadIdx.x & 31u) == (uint32_t)(__ffs(peers) - 1)) {
+        const uint32_t g = (uint32_t)__popc(peers);
+        const uint32_t old = s_atom_add(a, g << sh);
+        const uint32_t own = (old >> sh) & 0xffu, oth = (old >> (sh ^ 8u)) & 0xffu;
+        b32 += g * own + ((g * (g - 1u)) >> 1);
+        u32 += g * oth;
+      }
+      if (KEEP) touched[j] = a;
+      return;
+    }
+#endif
     if (W == 8 && !KG) {
       // the increment selects this wedge's own byte; a byte dot product (IDP4A) of the old
       // word with it adds the own count, with the end vertex's other byte the other count
