@@ -59,6 +59,20 @@ __device__ __forceinline__ uint32_t wedge_class(uint32_t w, uint32_t sg) {
   return ((w ^ sg) >> 31) ? 2u : (sg >> 31);
 }
 
+// the inline closing of one wedge of class t on an end vertex that held (a, b, d):
+// C(t,t) += own count, (t, t') += the other counts -- branch-free (selects)
+__device__ __forceinline__ void add_class(uint32_t t, uint32_t a, uint32_t b, uint32_t d, unsigned long long& c0,
+                                          unsigned long long& c1, unsigned long long& c2, unsigned long long& c3,
+                                          unsigned long long& c4, unsigned long long& c5) {
+  const bool p = t == 0u, m = t == 1u, x = t == 2u;
+  c0 += p ? a : 0u;
+  c2 += m ? b : 0u;
+  c3 += x ? d : 0u;
+  c1 += p ? b : (m ? a : 0u);
+  c4 += p ? d : (x ? a : 0u);
+  c5 += m ? d : (x ? b : 0u);
+}
+
 // classification, pp | mm << 10 | pm << 20 per end vertex (deg u <= 1023)
 struct OpClsC10 {
   uint32_t rb;
@@ -67,19 +81,7 @@ struct OpClsC10 {
     const uint32_t t = wedge_class(w, sg);
     const uint32_t old = s_atom_add(rb + (w << 2), 1u << (10u * t));
     const uint32_t a = old & 1023u, b = (old >> 10) & 1023u, d = old >> 20;
-    if (t == 0u) {  // pp: C(pp,2) += pp, pp*mm += mm, pp*pm += pm
-      c0 += a;
-      c1 += b;
-      c4 += d;
-    } else if (t == 1u) {  // mm
-      c2 += b;
-      c1 += a;
-      c5 += d;
-    } else {  // pm
-      c3 += d;
-      c4 += a;
-      c5 += b;
-    }
+    add_class(t, a, b, d, c0, c1, c2, c3, c4, c5);
   }
   __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
     chunk_by_wedge(*this, wv, sg, m);
@@ -132,19 +134,7 @@ struct OpClsHash {
     }
     const uint32_t old = atomicAdd(&tab[2u * h + 1u], 1u << (10u * t));
     const uint32_t a = old & 1023u, b = (old >> 10) & 1023u, d = old >> 20;
-    if (t == 0u) {
-      c0 += a;
-      c1 += b;
-      c4 += d;
-    } else if (t == 1u) {
-      c2 += b;
-      c1 += a;
-      c5 += d;
-    } else {
-      c3 += d;
-      c4 += a;
-      c5 += b;
-    }
+    add_class(t, a, b, d, c0, c1, c2, c3, c4, c5);
   }
   __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
     chunk_by_wedge(*this, wv, sg, m);
@@ -168,7 +158,8 @@ struct ExtSmem {
 // about K / 2 wedges in a shared-memory hash (OpClsHash): few rounds over sparse ranges.
 template <int T, int MODE>
 __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uint32_t rb, uint32_t re,
-                           unsigned long long (&acc)[12], uint32_t& ovf, unsigned long long& work) {
+                           unsigned long long w_a, unsigned long long (&acc)[12], uint32_t& ovf,
+                           unsigned long long& work) {
   const uint32_t deg = re - rb;
   const bool wide = deg > 1023u;
   const uint32_t wpv = wide ? 3u : 1u;  // words per end vertex
@@ -283,6 +274,12 @@ __device__ void ext_anchor(const ExtParams& P, const ExtSmem& S, uint32_t r, uin
       block_sync();  // every warp is done with this set-up's record arrays
       continue;
     }
+    if (b == 0u && hashing && nbands > 1u) {
+      // first hash-round width from the remaining wedges' average density (instead of
+      // doubling up from one column)
+      const unsigned long long rest = w_a > band_w ? w_a - band_w : 0ull, span_c = nbands - 1u;
+      width = (uint32_t)max(1ull, min(span_c, (unsigned long long)target * span_c / max(rest, 1ull)));
+    }
     b += nbw;
     if (band_w == 0ull) continue;
     uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
@@ -358,7 +355,8 @@ __global__ void __launch_bounds__(T, MINB) k_ext(ExtParams P) {
     if (threadIdx.x == 0) s_task = P.dynamic ? atomicAdd(P.queue, 1u) : next;
     const uint32_t gidx = P.part_index + t * P.part_count;
     const uint32_t r = P.dynamic ? P.order[gidx] : gidx;
-    if (P.awork[r] != 0ull) ext_anchor<T, MODE>(P, S, r, P.aoff[r], P.aoff[r + 1], acc, ovf, work);
+    const unsigned long long w_a = P.awork[r];
+    if (w_a != 0ull) ext_anchor<T, MODE>(P, S, r, P.aoff[r], P.aoff[r + 1], w_a, acc, ovf, work);
     block_sync();
   }
   // exact reduction: warp shuffle of the 128-bit values, one pair of atomics per warp

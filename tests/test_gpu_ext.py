@@ -25,7 +25,7 @@ def check_ext(arrays, rec, where, algos=ALGOS, flags=(0,)):
     gv = DeviceGraph.from_host(n_u, n_v, u, v, s, 0, SIDE_V)
     try:
         for algo in algos:
-            for fl in flags:  # 2: no classification hash rounds, 1024: no band table, 256: tiny repeat queue
+            for fl in flags:  # 2: no classification hash rounds, 1024: no band table
                 if "classes" in rec:
                     assert gu.classify(algo, flags=fl)[0] == rec["classes"], (where, algo, fl)
                 for key, val in rec.get("b2k", {}).items():
@@ -55,7 +55,7 @@ def test_corpora(gpu, golden, corpus):
 @pytest.mark.parametrize("key", ["1@1", "5@small"])
 def test_configs_vs_reference(gpu, golden, key):
     cfg = synth.golden_config(key)
-    check_ext((cfg.n_u, cfg.n_v, *synth.generate(cfg)), golden["configs"][key], key, flags=(0, 2, 256, 1024))
+    check_ext((cfg.n_u, cfg.n_v, *synth.generate(cfg)), golden["configs"][key], key, flags=(0, 2, 1024))
 
 
 @pytest.mark.parametrize("key", ["2@0.05", "3@0.002", "4@0.0002"])
@@ -65,7 +65,7 @@ def test_scaled_configs_vs_oracle(gpu, key):
     o = OracleGraph(*arrays)
     rec = {"classes": o.classify(), "b2k": {f"k{k}_{'uv'[side]}": o.count_2k(k, side)[0]
                                            for k in (3, 4) for side in (0, 1)}}
-    check_ext(arrays, rec, key, flags=(0, 2, 256, 1024))
+    check_ext(arrays, rec, key, flags=(0, 2, 1024))
 
 
 def test_wide_layouts_vs_oracle(gpu):
@@ -96,12 +96,12 @@ CONFIG2_CLASSES = {"coherent_pp_pp": 863675101, "coherent_pp_mm": 316150114, "co
 
 
 def test_config2_full_classification(gpu):
-    """Key-hash rounds (default), band tiles only (flags 2) and overflow-narrowed rounds
-    (flags 256) agree at full size; their sum is the total butterfly count."""
+    """Hash rounds (default) and band tiles only (flags 2), both algorithms, agree at full
+    size; the classes sum to the reference's balanced / unbalanced counts."""
     cfg = synth.golden_config("2@1")
     g = DeviceGraph.from_host(cfg.n_u, cfg.n_v, *synth.generate(cfg), 0, SIDE_U)
     try:
-        for algo, fl in ((ALGO_GBBCPP, 0), (ALGO_GBBC, 0), (ALGO_GBBCPP, 2), (ALGO_GBBCPP, 256)):
+        for algo, fl in ((ALGO_GBBCPP, 0), (ALGO_GBBC, 0), (ALGO_GBBCPP, 2)):
             assert g.classify(algo, flags=fl)[0] == CONFIG2_CLASSES, (algo, fl)
         c = CONFIG2_CLASSES  # balanced = same-parity wedge pairs; the reference's config-2 counts
         assert c["coherent_pp_pp"] + c["coherent_pp_mm"] + c["coherent_mm_mm"] + c["incoherent_pm_pm"] == 1840815365
