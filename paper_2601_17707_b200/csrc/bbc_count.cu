@@ -442,14 +442,14 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
         if (mode == kDense) {
           if (W == 32) {
             OpTileDense32 op{base};
-            walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+            walk_chunks<T, true>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
           } else {
             OpTileDense<W> op{base};
-            walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+            walk_chunks<T, true>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
           }
         } else {
           OpTileClose<W == 32 ? 16 : W, false, KG> op{base, &tb, &tu, P.k};
-          walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
+          walk_chunks<T, true>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
         }
       }
       block_sync();  // the next batch overwrites the record arrays
