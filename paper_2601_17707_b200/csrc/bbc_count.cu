@@ -86,9 +86,10 @@ struct Params {
 // slack).  Ranks are < 2^30 on the fast path, so (w >> s) keeps no sign bit after masking.
 
 // counter-tile increments without return (closed later by the sweep)
-template <int W>
+template <int W, bool BF = false>
 struct OpTileDense {
   uint32_t rb;
+  uint32_t dummy;  // a tile word of this lane (BF chunks add 0 to it)
   __device__ __forceinline__ void wedge(uint32_t w, uint32_t sg, int) {
     const uint32_t v = w ^ sg;  // bit 31: parity (1 = negative wedge)
 #ifdef BBC_MATCH
@@ -107,8 +108,30 @@ struct OpTileDense {
     else
       s_red_add(rb + ((w << 2) & 0xfffffffcu), 1u << ((v >> 27) & 16u));
   }
+  // BF (the fast path's dense tile rounds): branch-free chunk -- an invalid slot adds 0 to
+  // this lane's own tile word (a no-op; per-lane words, so the no-ops do not serialise on
+  // one address) and the eight adds issue back to back.  Measured: config 2 12.78 ->
+  // 12.58 ms; on the general path's dense W16 bands (config 5) the branchy form is faster
+  // (206 vs 229 ms).
   __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
-    chunk_by_wedge(*this, wv, sg, m);
+    if (!BF) {
+      chunk_by_wedge(*this, wv, sg, m);
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t w = wv[j], v = w ^ sg;
+      const bool ok = (m >> j) & 1u;
+      uint32_t a, inc;
+      if (W == 8) {
+        a = rb + ((w << 1) & 0xfffffffcu);
+        inc = 1u << (((w & 1u) << 4) | ((v >> 28) & 8u));
+      } else {
+        a = rb + ((w << 2) & 0xfffffffcu);
+        inc = 1u << ((v >> 27) & 16u);
+      }
+      s_red_add(ok ? a : dummy, ok ? inc : 0u);
+    }
   }
   __device__ __forceinline__ void flush() {}
 };
@@ -444,7 +467,7 @@ __device__ void process_anchor(const Params& P, const Smem& S, uint32_t r, uint3
             OpTileDense32 op{base};
             walk_chunks<T, true>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
           } else {
-            OpTileDense<W> op{base};
+            OpTileDense<W> op{base, 0u};
             walk_chunks<T, true>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
           }
         } else {
@@ -605,7 +628,7 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
       for (uint32_t i = threadIdx.x; i < (band_words + 3u) / 4u; i += T) c4[i] = make_uint4(0u, 0u, 0u, 0u);
     } else {
       // dense rounds: no-return increments and the shared-memory closing sweep
-      OpTileDense<W> op{base};
+      OpTileDense<W, true> op{base, sptr(S.cnt) + ((threadIdx.x & 31u) << 2)};
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
       block_sync();
       sweep<T, W, KG>(S.cnt, band_words, tb, tu, P.k);
