@@ -152,13 +152,14 @@ struct OpTileDense32 {
 // positive count to balanced and the old negative count to unbalanced, a - wedge the
 // reverse); 32-bit partial sums per pair (8 x 65535 < 2^32), flushed to 64 bits.  With
 // KEEP the touched word of each slot is kept (single-iteration rounds zero from it).
-template <int W, bool KEEP, bool KG = false>
+template <int W, bool KEEP, bool KG = false, bool BF = false>
 struct OpTileClose {
   uint32_t rb;
   unsigned long long *tb, *tu;
   uint32_t k = 2;  // KG: (2,k)-bicliques, a wedge on a bucket holding c adds C(c, k-1)
   uint32_t b32 = 0, u32 = 0;
   uint32_t touched[8];
+  uint32_t dummy = 0;  // BF: a tile word of this lane (invalid slots add 0 to it)
   __device__ __forceinline__ void add(uint32_t c, uint32_t other) {
     if (KG) {
       if (c >= k - 1u) add_k(*tb, *tu, binom_k(c, k - 1u));
@@ -213,7 +214,33 @@ struct OpTileClose {
       if (KEEP) touched[j] = a;
     }
   }
+  // BF (the fast path's tile rounds, k = 2): branch-free chunk -- an invalid slot adds 0 to
+  // the lane's own tile word and its return value is masked out of the sums
   __device__ __forceinline__ void chunk(const uint32_t (&wv)[8], uint32_t sg, uint32_t m) {
+    if (BF && !KG) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t w = wv[j], v = w ^ sg;
+        const bool ok = (m >> j) & 1u;
+        if (W == 8) {
+          const uint32_t hs = (w & 1u) << 4;
+          const uint32_t inc = ok ? 1u << (hs | ((v >> 28) & 8u)) : 0u;
+          const uint32_t a = ok ? rb + ((w << 1) & 0xfffffffcu) : dummy;
+          const uint32_t old = s_atom_add(a, inc);
+          b32 = __dp4a(old, inc, b32);
+          u32 = __dp4a(old, ok ? (0x101u << hs) ^ inc : 0u, u32);
+          if (KEEP) touched[j] = ok ? a : touched[j];
+        } else {
+          const uint32_t sh = (v >> 27) & 16u;
+          const uint32_t a = ok ? rb + ((w << 2) & 0xfffffffcu) : dummy;
+          const uint32_t old = s_atom_add(a, ok ? 1u << sh : 0u);
+          b32 += ok ? (old >> sh) & 0xffffu : 0u;
+          u32 += ok ? (old >> (sh ^ 16u)) & 0xffffu : 0u;
+          if (KEEP) touched[j] = ok ? a : touched[j];
+        }
+      }
+      return;
+    }
     chunk_by_wedge(*this, wv, sg, m);
   }
   __device__ __forceinline__ void flush() {
@@ -610,7 +637,8 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     if (ngroups <= (uint32_t)T) {
       // at most one chunk per thread: close inline and zero the touched words
       // from registers (no second pass over the tile or the adjacency)
-      OpTileClose<W, true, KG> op{base, &tb, &tu, P.k};
+      OpTileClose<W, true, KG, true> op{base, &tb, &tu, P.k};
+      op.dummy = sptr(S.cnt) + ((threadIdx.x & 31u) << 2);
 #pragma unroll
       for (int j = 0; j < 8; ++j) op.touched[j] = 0xffffffffu;
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
@@ -621,7 +649,8 @@ __device__ void process_anchor_fast(const Params& P, const Smem& S, uint32_t r, 
     } else if (bw < (unsigned long long)P.sweep_min * band_words && !(P.debug & 2048)) {
       // medium rounds: inline closing, then the tile is cleared with vector stores (a
       // closing sweep costs ~9 instructions per counter word, inline closing ~4 per wedge)
-      OpTileClose<W, false, KG> op{base, &tb, &tu, P.k};
+      OpTileClose<W, false, KG, true> op{base, &tb, &tu, P.k};
+      op.dummy = sptr(S.cnt) + ((threadIdx.x & 31u) << 2);
       walk_chunks<T>(P.adj, S.lo, S.hi, S.pfx, nb, ngroups, op);
       block_sync();
       uint4* c4 = reinterpret_cast<uint4*>(S.cnt);
